@@ -1,0 +1,184 @@
+/*
+ * klnmf.h -- C ABI of the B200-native SRCD hot path (libklnmf.so).
+ *
+ * Two layers:
+ *
+ *  1. Drop-in entry points with HOST pointers in the reference's own layout
+ *     (factors (r, n_items) C-order fp64, CSC with int64 indices).  They are
+ *     exactly the native functions the reference Python package calls, so a
+ *     maintainer binds them with ctypes in place of the numba kernels
+ *     (INTEGRATION.md shows the stub):
+ *       klnmf_sweep_range   replaces _kernels.sweep_range  (pkg/src/klnmf/_kernels.py:123-144)
+ *       klnmf_kl_data_term  replaces _kernels.kl_data_term (pkg/src/klnmf/_kernels.py:147-160)
+ *       klnmf_row_sums      replaces DenseFactor.row_sums  (pkg/src/klnmf/sparse.py:194-196)
+ *     Results are bit-identical to the reference (fp64 oracle mode).
+ *
+ *  2. Device-resident entry points (DEVICE pointers + a cudaStream_t passed as
+ *     void*) used by the Python host layer's plan (paper_1604_04026_b200/plan.py),
+ *     which replaces the reference's sweep()/factorize() loop
+ *     (pkg/src/klnmf/solver.py:165-216, :237-326): device CSC->CSR build and nnz
+ *     bucketing, row sums, the subproblem solver kernels (fp64 exact mode and
+ *     fp32-storage throughput mode), the KL objective and factor statistics.
+ *
+ * Device layout: a factor with n items and rank r is stored item-major as
+ * (n, rp) with rp = r rounded up to a multiple of 4 (zero padding), so the
+ * gather of one stored entry's fixed-factor vector is one contiguous run.
+ * Columns are kept in VISIT ORDER of the current outer iteration: position tt
+ * holds the coordinate ids[tt] (solver.py:287 shares one permutation across
+ * both sweeps and all subproblems), so the solver streams each row front to
+ * back.  perm_in/perm_out maps re-order a moving row on the fly.
+ *
+ * Every function returns 0 on success or a CUDA error code; the message is
+ * available from klnmf_last_error().  Kernels never raise on numerical
+ * trouble: like the reference (numba error_model="numpy") they produce IEEE
+ * inf/nan.  Nothing here has a CPU fallback.
+ */
+#ifndef KLNMF_H
+#define KLNMF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KLNMF_ABI_VERSION 1
+
+/* stats slots, _kernels.py:16-21 */
+#define KLNMF_STAT_CAP_HITS 0
+#define KLNMF_STAT_DEGENERATE 1
+#define KLNMF_STAT_INNER_ITERS 2
+#define KLNMF_STAT_PASSES 3
+#define KLNMF_STATS_LEN 4
+
+int klnmf_abi_version(void);
+const char *klnmf_last_error(void);
+
+/* ------------------------------------------------------------------ */
+/* 1. Drop-in host entry points (reference layout, fp64, bit-exact).   */
+
+/* _kernels.sweep_range(col_ptr, row_idx, values, at, sum_a, moving, j_lo, j_hi,
+ *   ids, alpha, beta, eps_grad, eps_x, eps_div, inner_cap, ax_buf, x_buf, stats)
+ * (_kernels.py:124-127).  The numba signature takes shapes from the arrays;
+ * here they are explicit (n_fix = at.shape[1], n_mov = moving.shape[1],
+ * r = at.shape[0]).  ax_buf/x_buf are not needed (device scratch).  Columns
+ * j_lo..j_hi-1 of moving (r, n_mov) are updated in place; stats (int64[4])
+ * are ACCUMULATED like the reference does. */
+int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                      const double *at, const double *sum_a, double *moving, int64_t j_lo,
+                      int64_t j_hi, const int64_t *ids, double alpha, double beta,
+                      double eps_grad, double eps_x, double eps_div, int64_t inner_cap,
+                      int64_t r, int64_t n_fix, int64_t n_mov, int64_t *stats);
+
+/* _kernels.kl_data_term(col_ptr, row_idx, values, w, f, eps_div) (_kernels.py:148):
+ * sum over stored entries of v*log(v/((W^T F)_ij + eps)) - v.  w is (r, n_rows),
+ * f is (r, n_cols).  Result in *out. */
+int klnmf_kl_data_term(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                       const double *w, const double *f, double eps_div, int64_t r,
+                       int64_t n_rows, int64_t n_cols, double *out);
+
+/* DenseFactor.row_sums (sparse.py:194-196): out[k] = sum_i factor[k, i] with
+ * numpy's pairwise summation order (bit-identical). factor is (r, n). */
+int klnmf_row_sums(const double *factor, int64_t r, int64_t n, double *out);
+
+/* ------------------------------------------------------------------ */
+/* 2. Device-resident entry points.                                    */
+
+/* One oriented view of V: CSC of V (F-side) or CSC of V^T (= CSR of V, W-side). */
+typedef struct {
+    const int64_t *ptr;   /* n_mov + 1 */
+    const int32_t *idx;   /* nnz, index into the fixed factor */
+    const void *val;      /* nnz, float (fp32 mode) or double (exact mode) */
+    int64_t n_fix;
+    int64_t n_mov;
+    int64_t nnz;
+} klnmf_side_t;
+
+/* Solver arguments shared by both precisions.  Pointers are device pointers. */
+typedef struct {
+    klnmf_side_t side;
+    const void *fixed;        /* (n_fix, rp) visit order, float or double */
+    void *moving;             /* (n_mov, rp), float or double, in/out */
+    const double *sum_pos;    /* rp: fixed-factor row sums by position */
+    const int32_t *perm_in;   /* rp: moving row position holding visit position tt */
+    const int32_t *perm_out;  /* rp: moving row position to write visit position tt */
+    const int32_t *nat_pos;   /* r: visit position of natural coordinate k (exact mode) */
+    const int32_t *items;     /* subproblem (moving item) ids to solve */
+    int64_t n_items;
+    /* fp32 mode: maintained products carried between half-steps */
+    const int32_t *tmap;      /* nnz: index into t_in of each entry (NULL = identity) */
+    const double *t_in;
+    double *t_out;            /* nnz, entry order of this side */
+    double *scratch;          /* exact mode: nnz doubles; fp32 streaming bucket: 2*nnz */
+    int32_t r;
+    int32_t rp;
+    double alpha, beta, eps_grad, eps_x, eps_div;
+    int64_t inner_cap;
+    unsigned long long *stats; /* device, KLNMF_STATS_LEN, accumulated */
+} klnmf_solve_args_t;
+
+/* exact fp64 solver (bit-identical to _kernels.sweep_range, one warp per subproblem) */
+int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream);
+
+/* fp32-storage / fp64-arithmetic solver.  kernel_id selects the bucket kernel:
+ * lanes-per-subproblem L and entries-per-lane NPL (klnmf_fast_kernel_info). */
+int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, void *stream);
+int klnmf_fast_kernel_count(void);
+/* capacity (max nnz per subproblem) and lanes of kernel_id; capacity < 0 = unbounded */
+int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t *lanes, int32_t *npl);
+
+/* row sums of a device factor by position (n_items, rp): exact = numpy pairwise over
+ * fp64 items in order; fast = deterministic fp64 two-level sum of fp32 items. */
+int klnmf_row_sums_exact(const double *fac, int64_t n_items, int32_t rp, int32_t r,
+                         double *out, void *stream);
+int klnmf_row_sums_fast(const float *fac, int64_t n_items, int32_t rp, int32_t r,
+                        double *out, void *stream);
+
+/* reference layout (r, n) fp64 <-> device layout (n, rp) in visit order.
+ * order[tt] = natural coordinate stored at position tt (tt < r). */
+int klnmf_layout_to_device(const double *src, int64_t r, int64_t n, const int32_t *order,
+                           int32_t rp, void *dst, int fp32, void *stream);
+int klnmf_layout_from_device(const void *src, int64_t r, int64_t n, const int32_t *order,
+                             int32_t rp, int fp32, double *dst, void *stream);
+
+/* CSC (ptr/idx/val) -> CSC of the transpose, plus both entry maps:
+ * map_t2o[q'] = position in the input of output entry q', map_o2t = inverse.
+ * Stable (rows ascending, then columns ascending), as sparse.py:146-154. */
+int klnmf_transpose(const int64_t *ptr, const int32_t *idx, const void *val, int val_bytes,
+                    int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t *ptr_t,
+                    int32_t *idx_t, void *val_t, int32_t *map_t2o, int32_t *map_o2t,
+                    void *stream);
+
+/* COO -> CSC (sorted by column then row, as sparse.py:92-124); values must be
+ * > 0 (zeros dropped by the caller).  *dup_flag != 0 reports a duplicate. */
+int klnmf_coo_to_csc(const int32_t *rows, const int32_t *cols, const void *vals, int val_bytes,
+                     int64_t nnz, int64_t n_rows, int64_t n_cols, int64_t *ptr, int32_t *idx,
+                     void *val, int32_t *dup_flag, void *stream);
+
+/* nnz bucketing of subproblems j in [j_lo, j_hi): items sorted by nnz descending;
+ * bucket_start[b] = first slot of bucket b where bucket b holds nnz <= bounds[b]
+ * (bounds ascending, last bound may be INT64_MAX).  n_bounds <= 32. */
+int klnmf_bucketize(const int64_t *ptr, int64_t j_lo, int64_t j_hi, const int64_t *bounds,
+                    int n_bounds, int32_t *items, int64_t *bucket_count_host, void *stream);
+
+/* fp32 mode: t[q] = <W_i, F_j> (fp64, natural order) for every entry of side. */
+int klnmf_init_t(const klnmf_side_t *side, const float *fixed, const float *moving, int32_t rp,
+                 const int32_t *fixed_pos, const int32_t *moving_pos, int32_t r, double *t,
+                 void *stream);
+
+/* KL data term over the CSC of V: sum v*log(v/(d+eps)) - v with d = <W_i,F_j>
+ * accumulated in natural coordinate order (wpos/fpos map coordinate -> position).
+ * fp32 selects float factors.  Deterministic.  Result (fp64) in *out_host. */
+int klnmf_kl_data_term_dev(const klnmf_side_t *csc, const void *w, const void *f, int32_t rp,
+                           const int32_t *wpos, const int32_t *fpos, int32_t r, int fp32,
+                           double eps_div, double *out_host, void *stream);
+
+/* factor statistics over the r real columns: out_host[0] = sum x^2, [1] = sum x,
+ * [2] = number of exact zeros (as double).  Deterministic. */
+int klnmf_factor_stats(const void *fac, int64_t n_items, int32_t rp, int32_t r, int fp32,
+                       double *out_host, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KLNMF_H */

@@ -1,0 +1,410 @@
+/*
+ * klnmf_oracle.c -- CPU restatement of the reference SRCD hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the CUDA
+ * path: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it.  The product (paper_1604_04026_b200)
+ * never links, imports or calls it; there is no CPU fallback.
+ *
+ * Every function restates one numba kernel of the reference package
+ * (klnmf, /root/reference/pkg/src/klnmf) with the same operation order:
+ * numba emits no FMA and no fast-math (SURVEY.md finding 3), so this file is
+ * compiled with -ffp-contract=off and without -ffast-math, and the results
+ * are bit-identical to the reference (pinned by tests/test_oracle_golden.py
+ * against fixtures generated from the reference itself).
+ *
+ *   oracle_sweep_range_dense    _kernels.py:123-144 (+ solve_column :53-120,
+ *                               _grad_hess :24-36, compute_ax :39-50), with the
+ *                               reference's dense length-n_fix maintained product
+ *   oracle_sweep_range_support  the same algorithm with the maintained product
+ *                               kept only on the column's support S (bitwise
+ *                               identical: every ax[i] evolves independently and
+ *                               is only read at S -- SURVEY.md finding 2)
+ *   oracle_sweep                the reference's sweep() thread pool
+ *                               (solver.py:165-216): equal-count column chunks
+ *   oracle_kl_data_term         _kernels.py:147-160
+ *   oracle_row_sums             DenseFactor.row_sums (sparse.py:194-196) =
+ *                               numpy's pairwise summation (SURVEY.md finding 8)
+ *   oracle_sweep_fp32           the fp32-storage / fp64-arithmetic mode of the
+ *                               CUDA path, restated on
+ *                               the device layout so sampled subproblems can be
+ *                               compared one by one at full problem sizes
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define STAT_CAP_HITS 0   /* _kernels.py:17 */
+#define STAT_DEGENERATE 1 /* _kernels.py:18 */
+#define STAT_INNER_ITERS 2/* _kernels.py:19 */
+#define STAT_PASSES 3     /* _kernels.py:20 */
+
+/* ------------------------------------------------------------------ */
+/* _grad_hess, _kernels.py:24-36.  ax is indexed by row (dense) or by the
+ * position p inside the column (support variant, ax_is_local != 0).      */
+static inline void grad_hess(int64_t k, const int64_t *v_idx, const double *v_val, int64_t s,
+                             const double *at, int64_t n_fix, const double *ax, int ax_is_local,
+                             const double *sum_a, double x_k, double alpha, double beta,
+                             double eps_div, double *g_out, double *h_out) {
+    double g = sum_a[k] + alpha * x_k + beta;
+    double h = alpha;
+    const double *row = at + k * n_fix;
+    for (int64_t p = 0; p < s; ++p) {
+        double a = row[v_idx[p]];
+        if (a != 0.0) {
+            double q = a / (ax[ax_is_local ? p : v_idx[p]] + eps_div);
+            g -= v_val[p] * q;
+            h += v_val[p] * q * q;
+        }
+    }
+    *g_out = g;
+    *h_out = h;
+}
+
+/* compute_ax, _kernels.py:39-50: natural k order, exact zeros of x skipped. */
+static void compute_ax_dense(const double *at, int64_t r, int64_t n_fix, const double *x, double *ax) {
+    for (int64_t i = 0; i < n_fix; ++i) ax[i] = 0.0;
+    for (int64_t k = 0; k < r; ++k) {
+        double xk = x[k];
+        if (xk != 0.0) {
+            const double *row = at + k * n_fix;
+            for (int64_t i = 0; i < n_fix; ++i) ax[i] += xk * row[i];
+        }
+    }
+}
+
+static void compute_ax_support(const double *at, int64_t r, int64_t n_fix, const double *x,
+                               const int64_t *v_idx, int64_t s, double *t) {
+    for (int64_t p = 0; p < s; ++p) t[p] = 0.0;
+    for (int64_t k = 0; k < r; ++k) {
+        double xk = x[k];
+        if (xk != 0.0) {
+            const double *row = at + k * n_fix;
+            for (int64_t p = 0; p < s; ++p) t[p] += xk * row[v_idx[p]];
+        }
+    }
+}
+
+/* ax += delta * at[k], clamped at 0: _kernels.py:86-90 and :103-106. */
+static inline void update_ax(const double *at, int64_t k, int64_t n_fix, double delta, double *ax,
+                             int local, const int64_t *v_idx, int64_t s) {
+    const double *row = at + k * n_fix;
+    if (!local) {
+        for (int64_t i = 0; i < n_fix; ++i) {
+            ax[i] += delta * row[i];
+            if (ax[i] < 0.0) ax[i] = 0.0;
+        }
+    } else {
+        for (int64_t p = 0; p < s; ++p) {
+            ax[p] += delta * row[v_idx[p]];
+            if (ax[p] < 0.0) ax[p] = 0.0;
+        }
+    }
+}
+
+/* solve_column, _kernels.py:53-120 (max_passes as in the reference). */
+void oracle_solve_column(const int64_t *v_idx, const double *v_val, int64_t s, const double *at,
+                         int64_t r, int64_t n_fix, const double *sum_a, double *x, double *ax,
+                         int local, const int64_t *ids, double alpha, double beta, double eps_grad,
+                         double eps_x, double eps_div, int64_t inner_cap, int64_t max_passes,
+                         int64_t *stats) {
+    if (local)
+        compute_ax_support(at, r, n_fix, x, v_idx, s, ax);
+    else
+        compute_ax_dense(at, r, n_fix, x, ax);
+    for (int64_t pass = 0; pass < max_passes; ++pass) {
+        stats[STAT_PASSES] += 1;
+        int moved = 0;
+        for (int64_t tt = 0; tt < r; ++tt) {
+            int64_t k = ids[tt];
+            double x_enter = x[k];
+            double g, h;
+            grad_hess(k, v_idx, v_val, s, at, n_fix, ax, local, sum_a, x[k], alpha, beta, eps_div, &g, &h);
+            int64_t inner = 0;
+            while ((g < -eps_grad) || (fabs(g) > eps_grad && x[k] > eps_grad)) {
+                if (h <= 0.0) {
+                    if (g > 0.0) {
+                        double delta = -x[k];
+                        if (delta != 0.0) {
+                            update_ax(at, k, n_fix, delta, ax, local, v_idx, s);
+                            x[k] = 0.0;
+                        }
+                    } else {
+                        stats[STAT_DEGENERATE] += 1;
+                    }
+                    break;
+                }
+                double target = x[k] - g / h;
+                if (target < 0.0) target = 0.0;
+                double delta = target - x[k];
+                update_ax(at, k, n_fix, delta, ax, local, v_idx, s);
+                double xs = x[k];
+                x[k] = xs + delta;
+                inner += 1;
+                stats[STAT_INNER_ITERS] += 1;
+                if (fabs(delta) < eps_x * xs) break;
+                if (inner >= inner_cap) {
+                    stats[STAT_CAP_HITS] += 1;
+                    break;
+                }
+                grad_hess(k, v_idx, v_val, s, at, n_fix, ax, local, sum_a, x[k], alpha, beta, eps_div, &g, &h);
+            }
+            if (x[k] != x_enter) moved = 1;
+        }
+        if (!moved) break;
+    }
+}
+
+/* sweep_range, _kernels.py:123-144 (one pass per column).  at is (r, n_fix)
+ * C-order, moving is (r, n_mov) C-order, both fp64 -- the reference layout.
+ * ax_buf has n_fix entries (dense) or max column nnz entries (support).   */
+static void sweep_range_impl(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                             const double *at, int64_t r, int64_t n_fix, const double *sum_a,
+                             double *moving, int64_t n_mov, int64_t j_lo, int64_t j_hi,
+                             const int64_t *ids, double alpha, double beta, double eps_grad,
+                             double eps_x, double eps_div, int64_t inner_cap, double *ax_buf,
+                             double *x_buf, int64_t *stats, int local) {
+    for (int64_t j = j_lo; j < j_hi; ++j) {
+        for (int64_t k = 0; k < r; ++k) x_buf[k] = moving[k * n_mov + j];
+        int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
+        oracle_solve_column(row_idx + lo, values + lo, hi - lo, at, r, n_fix, sum_a, x_buf, ax_buf,
+                            local, ids, alpha, beta, eps_grad, eps_x, eps_div, inner_cap, 1, stats);
+        for (int64_t k = 0; k < r; ++k) moving[k * n_mov + j] = x_buf[k];
+    }
+}
+
+void oracle_sweep_range_dense(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                              const double *at, int64_t r, int64_t n_fix, const double *sum_a,
+                              double *moving, int64_t n_mov, int64_t j_lo, int64_t j_hi,
+                              const int64_t *ids, double alpha, double beta, double eps_grad,
+                              double eps_x, double eps_div, int64_t inner_cap, double *ax_buf,
+                              double *x_buf, int64_t *stats) {
+    sweep_range_impl(col_ptr, row_idx, values, at, r, n_fix, sum_a, moving, n_mov, j_lo, j_hi, ids,
+                     alpha, beta, eps_grad, eps_x, eps_div, inner_cap, ax_buf, x_buf, stats, 0);
+}
+
+void oracle_sweep_range_support(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                const double *at, int64_t r, int64_t n_fix, const double *sum_a,
+                                double *moving, int64_t n_mov, int64_t j_lo, int64_t j_hi,
+                                const int64_t *ids, double alpha, double beta, double eps_grad,
+                                double eps_x, double eps_div, int64_t inner_cap, double *ax_buf,
+                                double *x_buf, int64_t *stats) {
+    sweep_range_impl(col_ptr, row_idx, values, at, r, n_fix, sum_a, moving, n_mov, j_lo, j_hi, ids,
+                     alpha, beta, eps_grad, eps_x, eps_div, inner_cap, ax_buf, x_buf, stats, 1);
+}
+
+/* ------------------------------------------------------------------ */
+/* sweep(), solver.py:165-216: equal-count chunks (_chunk_bounds,
+ * solver.py:160-162 = np.linspace(0, n, workers+1).astype(int64)), one
+ * worker each, stats summed.  Results are worker-count invariant.       */
+typedef struct {
+    const int64_t *col_ptr, *row_idx;
+    const double *values, *at, *sum_a;
+    double *moving;
+    const int64_t *ids;
+    int64_t r, n_fix, n_mov, j_lo, j_hi, inner_cap, scratch;
+    double alpha, beta, eps_grad, eps_x, eps_div;
+    int local;
+    int64_t stats[4];
+} sweep_task_t;
+
+static void *sweep_worker(void *arg) {
+    sweep_task_t *t = (sweep_task_t *)arg;
+    double *ax = (double *)malloc(sizeof(double) * (size_t)(t->scratch > 0 ? t->scratch : 1));
+    double *x = (double *)malloc(sizeof(double) * (size_t)t->r);
+    sweep_range_impl(t->col_ptr, t->row_idx, t->values, t->at, t->r, t->n_fix, t->sum_a, t->moving,
+                     t->n_mov, t->j_lo, t->j_hi, t->ids, t->alpha, t->beta, t->eps_grad, t->eps_x,
+                     t->eps_div, t->inner_cap, ax, x, t->stats, t->local);
+    free(ax);
+    free(x);
+    return NULL;
+}
+
+int oracle_sweep(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                 const double *at, int64_t r, int64_t n_fix, const double *sum_a, double *moving,
+                 int64_t n_mov, const int64_t *ids, double alpha, double beta, double eps_grad,
+                 double eps_x, double eps_div, int64_t inner_cap, int n_workers, int local,
+                 int64_t *stats_out) {
+    if (n_workers < 1) n_workers = 1;
+    int64_t max_s = 0;
+    for (int64_t j = 0; j < n_mov; ++j) {
+        int64_t s = col_ptr[j + 1] - col_ptr[j];
+        if (s > max_s) max_s = s;
+    }
+    sweep_task_t *tasks = (sweep_task_t *)calloc((size_t)n_workers, sizeof(sweep_task_t));
+    pthread_t *th = (pthread_t *)calloc((size_t)n_workers, sizeof(pthread_t));
+    int n_tasks = 0;
+    for (int w = 0; w < n_workers; ++w) {
+        /* np.linspace(0, n, W+1).astype(int64): floor of w*n/W in fp64 */
+        int64_t a = (int64_t)((double)n_mov * (double)w / (double)n_workers);
+        int64_t b = (w + 1 == n_workers) ? n_mov : (int64_t)((double)n_mov * (double)(w + 1) / (double)n_workers);
+        if (b <= a) continue;
+        sweep_task_t *t = &tasks[n_tasks++];
+        t->col_ptr = col_ptr; t->row_idx = row_idx; t->values = values; t->at = at; t->sum_a = sum_a;
+        t->moving = moving; t->ids = ids; t->r = r; t->n_fix = n_fix; t->n_mov = n_mov;
+        t->j_lo = a; t->j_hi = b; t->inner_cap = inner_cap; t->scratch = local ? max_s : n_fix;
+        t->alpha = alpha; t->beta = beta; t->eps_grad = eps_grad; t->eps_x = eps_x; t->eps_div = eps_div;
+        t->local = local;
+    }
+    if (n_tasks == 1) {
+        sweep_worker(&tasks[0]);
+    } else {
+        for (int i = 0; i < n_tasks; ++i) pthread_create(&th[i], NULL, sweep_worker, &tasks[i]);
+        for (int i = 0; i < n_tasks; ++i) pthread_join(th[i], NULL);
+    }
+    for (int i = 0; i < n_tasks; ++i)
+        for (int q = 0; q < 4; ++q) stats_out[q] += tasks[i].stats[q];
+    free(tasks);
+    free(th);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* kl_data_term, _kernels.py:147-160: serial over columns then nonzeros. */
+double oracle_kl_data_term(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                           int64_t n_cols, const double *w, int64_t n_rows, const double *f,
+                           int64_t r, double eps_div) {
+    double total = 0.0;
+    for (int64_t j = 0; j < n_cols; ++j) {
+        for (int64_t p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+            int64_t i = row_idx[p];
+            double d = 0.0;
+            for (int64_t k = 0; k < r; ++k) d += w[k * n_rows + i] * f[k * n_cols + j];
+            double v = values[p];
+            total += v * log(v / (d + eps_div)) - v;
+        }
+    }
+    return total;
+}
+
+/* numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h.src), the algorithm
+ * behind DenseFactor.row_sums (sparse.py:194-196); PW_BLOCKSIZE 128, 8-way
+ * unrolled leaves.  Matches numpy 2.3 bit for bit (tests/test_oracle_golden). */
+static double pairwise_sum(const double *a, int64_t n, int64_t stride) {
+    if (n < 8) {
+        double res = 0.;
+        for (int64_t i = 0; i < n; ++i) res += a[i * stride];
+        return res;
+    } else if (n <= 128) {
+        double r[8], res;
+        int64_t i;
+        for (int q = 0; q < 8; ++q) r[q] = a[q * stride];
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int q = 0; q < 8; ++q) r[q] += a[(i + q) * stride];
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i * stride];
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return pairwise_sum(a, n2, stride) + pairwise_sum(a + n2 * stride, n - n2, stride);
+    }
+}
+
+void oracle_row_sums(const double *factor, int64_t r, int64_t n, double *out) {
+    for (int64_t k = 0; k < r; ++k) out[k] = pairwise_sum(factor + k * n, n, 1);
+}
+
+/* ------------------------------------------------------------------ */
+/* fp32-storage mode: factors are fp32 values stored item-major
+ * in visit order (row i of `fixed` is the r-vector of item i, column tt is the
+ * coordinate visited tt-th), arithmetic is fp64, the maintained product t of
+ * every stored entry is carried between half-steps, and each Newton step
+ * rounds the coordinate to fp32 so t stays consistent with the stored factor.
+ * The gradient is the reference's _grad_hess (_kernels.py:24-36) rewritten
+ * with per-entry u = v/(t+eps), z = u/(t+eps): g = sum_a + alpha*x + beta -
+ * sum(u*a), h = alpha + sum(z*a*a).  The control flow is solve_column's
+ * (_kernels.py:73-118) verbatim.                                            */
+static inline double round_f32(double x) { return (double)(float)x; }
+
+void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val, int64_t n_mov,
+                       const float *fixed, int64_t rp, int64_t r, const double *sum_fixed,
+                       float *moving, double *t, const int64_t *items, int64_t n_items,
+                       double alpha, double beta, double eps_grad, double eps_x, double eps_div,
+                       int64_t inner_cap, int64_t *stats) {
+    (void)n_mov;
+    int64_t cap_s = 0;
+    for (int64_t q = 0; q < n_items; ++q) {
+        int64_t j = items ? items[q] : q;
+        int64_t s = ptr[j + 1] - ptr[j];
+        if (s > cap_s) cap_s = s;
+    }
+    double *u = (double *)malloc(sizeof(double) * (size_t)(cap_s + 1));
+    double *z = (double *)malloc(sizeof(double) * (size_t)(cap_s + 1));
+    for (int64_t q = 0; q < n_items; ++q) {
+        int64_t j = items ? items[q] : q;
+        int64_t lo = ptr[j], s = ptr[j + 1] - lo;
+        double *tj = t + lo;
+        for (int64_t p = 0; p < s; ++p) {
+            double rinv = 1.0 / (tj[p] + eps_div);
+            u[p] = (double)val[lo + p] * rinv;
+            z[p] = u[p] * rinv;
+        }
+        stats[STAT_PASSES] += 1;
+        for (int64_t tt = 0; tt < r; ++tt) {
+            double x = (double)moving[j * rp + tt];
+            double g, h;
+#define EVAL()                                                            \
+    do {                                                                  \
+        double gp = 0.0, hp = 0.0;                                        \
+        for (int64_t p = 0; p < s; ++p) {                                 \
+            double a = (double)fixed[(int64_t)idx[lo + p] * rp + tt];     \
+            if (a != 0.0) {                                               \
+                gp += u[p] * a;                                           \
+                hp += (z[p] * a) * a;                                     \
+            }                                                             \
+        }                                                                 \
+        g = sum_fixed[tt] + alpha * x + beta - gp;                        \
+        h = alpha + hp;                                                   \
+    } while (0)
+            EVAL();
+            int64_t inner = 0;
+            while ((g < -eps_grad) || (fabs(g) > eps_grad && x > eps_grad)) {
+                double delta;
+                int stop = 0;
+                if (h <= 0.0) {
+                    if (g > 0.0 && x != 0.0) {
+                        delta = -x;
+                        x = 0.0;
+                    } else {
+                        if (!(g > 0.0)) stats[STAT_DEGENERATE] += 1;
+                        delta = 0.0;
+                    }
+                    stop = 1;
+                } else {
+                    double target = x - g / h;
+                    if (target < 0.0) target = 0.0;
+                    double xn = round_f32(target);
+                    delta = xn - x;
+                    double xs = x;
+                    x = xn;
+                    inner += 1;
+                    stats[STAT_INNER_ITERS] += 1;
+                    if (fabs(delta) < eps_x * xs) stop = 1;
+                    else if (inner >= inner_cap) { stats[STAT_CAP_HITS] += 1; stop = 1; }
+                }
+                if (delta != 0.0) {
+                    for (int64_t p = 0; p < s; ++p) {
+                        double a = (double)fixed[(int64_t)idx[lo + p] * rp + tt];
+                        if (a != 0.0) {
+                            double tn = tj[p] + delta * a;
+                            if (tn < 0.0) tn = 0.0;
+                            tj[p] = tn;
+                            double rinv = 1.0 / (tn + eps_div);
+                            u[p] = (double)val[lo + p] * rinv;
+                            z[p] = u[p] * rinv;
+                        }
+                    }
+                }
+                if (stop) break;
+                EVAL();
+            }
+#undef EVAL
+            moving[j * rp + tt] = (float)x;
+        }
+    }
+    free(u);
+    free(z);
+}

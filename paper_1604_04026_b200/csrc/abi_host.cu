@@ -1,0 +1,252 @@
+// C-ABI plumbing and the host-pointer drop-in entry points.
+//
+// klnmf_sweep_range / klnmf_kl_data_term / klnmf_row_sums take the exact
+// arguments of the reference's native functions (_kernels.py:123-160,
+// sparse.py:194-196) as host arrays in the reference layout, stage them on the
+// device, run the fp64 exact-mode kernels and copy the results back.  They are
+// what a maintainer binds with ctypes in place of the numba kernels
+// (INTEGRATION.md).  Every call is self-contained (own stream, own buffers).
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace klnmf {
+
+static thread_local char g_err[512] = "";
+
+int set_error(cudaError_t err, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorString(err), cudaGetErrorName(err));
+    return (int)err;
+}
+
+int set_error_msg(int code, const char *msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+int row_sums_ref_layout(const double *fac_dev, int64_t r, int64_t n, double *out_dev, cudaStream_t st);
+
+namespace {
+
+__global__ void i64_to_i32(const int64_t *src, int64_t n, int32_t *dst) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        dst[q] = (int32_t)src[q];
+}
+
+__global__ void iota_from(int32_t *dst, int64_t n, int64_t start) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        dst[q] = (int32_t)(start + q);
+}
+
+inline unsigned grid_for(int64_t total) {
+    int64_t b = (total + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > 148 * 32) b = 148 * 32;
+    return (unsigned)b;
+}
+
+// RAII bundle of device allocations for one host call.
+struct DevBufs {
+    std::vector<void *> ptrs;
+    cudaStream_t st = nullptr;
+    ~DevBufs() {
+        for (void *p : ptrs) cudaFree(p);
+        if (st) cudaStreamDestroy(st);
+    }
+    template <typename T>
+    cudaError_t alloc(T **p, size_t count) {
+        void *q = nullptr;
+        cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+        if (e == cudaSuccess) ptrs.push_back(q);
+        *p = static_cast<T *>(q);
+        return e;
+    }
+};
+
+inline int32_t round_rp(int64_t r) { return (int32_t)((r + 3) / 4 * 4); }
+
+}  // namespace
+}  // namespace klnmf
+
+using namespace klnmf;
+
+extern "C" int klnmf_abi_version(void) { return KLNMF_ABI_VERSION; }
+
+extern "C" const char *klnmf_last_error(void) { return g_err; }
+
+extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                 const double *at, const double *sum_a, double *moving, int64_t j_lo, int64_t j_hi,
+                                 const int64_t *ids, double alpha, double beta, double eps_grad, double eps_x,
+                                 double eps_div, int64_t inner_cap, int64_t r, int64_t n_fix, int64_t n_mov,
+                                 int64_t *stats) {
+    if (r < 1 || n_fix < 0 || n_mov < 0 || j_lo < 0 || j_hi > n_mov)
+        return set_error_msg(1, "klnmf_sweep_range: bad shape or column range");
+    if (j_hi <= j_lo) return 0;
+    // ids must be a permutation of 0..r-1 (solver.py:287 draws rng.permutation(r))
+    std::vector<int32_t> order(r), nat(r, -1);
+    for (int64_t t = 0; t < r; ++t) {
+        const int64_t k = ids[t];
+        if (k < 0 || k >= r || nat[k] >= 0) return set_error_msg(1, "klnmf_sweep_range: ids must be a permutation");
+        order[t] = (int32_t)k;
+        nat[k] = (int32_t)t;
+    }
+    const int64_t nnz = col_ptr[n_mov];
+    if (nnz >= INT32_MAX) return set_error_msg(1, "klnmf_sweep_range: nnz must be < 2^31");
+    const int32_t rp = round_rp(r);
+    std::vector<double> sum_pos(rp, 0.0);
+    std::vector<int32_t> ident(rp);
+    for (int64_t t = 0; t < r; ++t) sum_pos[t] = sum_a[order[t]];
+    for (int t = 0; t < rp; ++t) ident[t] = t;
+
+    DevBufs B;
+    KLNMF_CHECK(cudaStreamCreateWithFlags(&B.st, cudaStreamNonBlocking));
+    cudaStream_t st = B.st;
+    int64_t *d_ptr, *d_row64;
+    int32_t *d_idx, *d_order, *d_nat, *d_ident, *d_items;
+    double *d_val, *d_at, *d_mov_ref, *d_fixed, *d_moving, *d_sum, *d_scratch;
+    unsigned long long *d_stats;
+    KLNMF_CHECK(B.alloc(&d_ptr, n_mov + 1));
+    KLNMF_CHECK(B.alloc(&d_row64, nnz));
+    KLNMF_CHECK(B.alloc(&d_idx, nnz));
+    KLNMF_CHECK(B.alloc(&d_val, nnz));
+    KLNMF_CHECK(B.alloc(&d_at, r * n_fix));
+    KLNMF_CHECK(B.alloc(&d_mov_ref, r * n_mov));
+    KLNMF_CHECK(B.alloc(&d_fixed, (int64_t)rp * n_fix));
+    KLNMF_CHECK(B.alloc(&d_moving, (int64_t)rp * n_mov));
+    KLNMF_CHECK(B.alloc(&d_sum, rp));
+    KLNMF_CHECK(B.alloc(&d_scratch, nnz));
+    KLNMF_CHECK(B.alloc(&d_order, rp));
+    KLNMF_CHECK(B.alloc(&d_nat, rp));
+    KLNMF_CHECK(B.alloc(&d_ident, rp));
+    KLNMF_CHECK(B.alloc(&d_items, j_hi - j_lo));
+    KLNMF_CHECK(B.alloc(&d_stats, KLNMF_STATS_LEN));
+
+    KLNMF_CHECK(cudaMemcpyAsync(d_ptr, col_ptr, sizeof(int64_t) * (n_mov + 1), cudaMemcpyHostToDevice, st));
+    if (nnz > 0) {
+        KLNMF_CHECK(cudaMemcpyAsync(d_row64, row_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+        KLNMF_CHECK(cudaMemcpyAsync(d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+        i64_to_i32<<<grid_for(nnz), 256, 0, st>>>(d_row64, nnz, d_idx);
+        KLNMF_CHECK_LAUNCH("i64_to_i32");
+    }
+    if (r * n_fix > 0)
+        KLNMF_CHECK(cudaMemcpyAsync(d_at, at, sizeof(double) * r * n_fix, cudaMemcpyHostToDevice, st));
+    if (r * n_mov > 0)
+        KLNMF_CHECK(cudaMemcpyAsync(d_mov_ref, moving, sizeof(double) * r * n_mov, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * r, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_nat, nat.data(), sizeof(int32_t) * r, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_ident, ident.data(), sizeof(int32_t) * rp, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_sum, sum_pos.data(), sizeof(double) * rp, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * KLNMF_STATS_LEN, st));
+    iota_from<<<grid_for(j_hi - j_lo), 256, 0, st>>>(d_items, j_hi - j_lo, j_lo);
+    KLNMF_CHECK_LAUNCH("iota_from");
+    int rc = klnmf_layout_to_device(d_at, r, n_fix, d_order, rp, d_fixed, 0, st);
+    if (rc) return rc;
+    rc = klnmf_layout_to_device(d_mov_ref, r, n_mov, d_order, rp, d_moving, 0, st);
+    if (rc) return rc;
+
+    klnmf_solve_args_t a;
+    memset(&a, 0, sizeof(a));
+    a.side.ptr = d_ptr;
+    a.side.idx = d_idx;
+    a.side.val = d_val;
+    a.side.n_fix = n_fix;
+    a.side.n_mov = n_mov;
+    a.side.nnz = nnz;
+    a.fixed = d_fixed;
+    a.moving = d_moving;
+    a.sum_pos = d_sum;
+    a.perm_in = d_ident;
+    a.perm_out = d_ident;
+    a.nat_pos = d_nat;
+    a.items = d_items;
+    a.n_items = j_hi - j_lo;
+    a.scratch = d_scratch;
+    a.r = (int32_t)r;
+    a.rp = rp;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.eps_grad = eps_grad;
+    a.eps_x = eps_x;
+    a.eps_div = eps_div;
+    a.inner_cap = inner_cap;
+    a.stats = d_stats;
+    rc = klnmf_solve_exact(&a, st);
+    if (rc) return rc;
+    rc = klnmf_layout_from_device(d_moving, r, n_mov, d_order, rp, 0, d_mov_ref, st);
+    if (rc) return rc;
+    unsigned long long hs[KLNMF_STATS_LEN];
+    if (r * n_mov > 0)
+        KLNMF_CHECK(cudaMemcpyAsync(moving, d_mov_ref, sizeof(double) * r * n_mov, cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(cudaStreamSynchronize(st));
+    for (int q = 0; q < KLNMF_STATS_LEN; ++q) stats[q] += (int64_t)hs[q];
+    return 0;
+}
+
+extern "C" int klnmf_kl_data_term(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                  const double *w, const double *f, double eps_div, int64_t r, int64_t n_rows,
+                                  int64_t n_cols, double *out) {
+    if (r < 1 || n_rows < 0 || n_cols < 0) return set_error_msg(1, "klnmf_kl_data_term: bad shape");
+    const int64_t nnz = col_ptr[n_cols];
+    if (nnz >= INT32_MAX) return set_error_msg(1, "klnmf_kl_data_term: nnz must be < 2^31");
+    const int32_t rp = round_rp(r);
+    std::vector<int32_t> ident(rp);
+    for (int t = 0; t < rp; ++t) ident[t] = t;
+    DevBufs B;
+    KLNMF_CHECK(cudaStreamCreateWithFlags(&B.st, cudaStreamNonBlocking));
+    cudaStream_t st = B.st;
+    int64_t *d_ptr, *d_row64;
+    int32_t *d_idx, *d_ident;
+    double *d_val, *d_w, *d_f, *d_wl, *d_fl;
+    KLNMF_CHECK(B.alloc(&d_ptr, n_cols + 1));
+    KLNMF_CHECK(B.alloc(&d_row64, nnz));
+    KLNMF_CHECK(B.alloc(&d_idx, nnz));
+    KLNMF_CHECK(B.alloc(&d_val, nnz));
+    KLNMF_CHECK(B.alloc(&d_w, r * n_rows));
+    KLNMF_CHECK(B.alloc(&d_f, r * n_cols));
+    KLNMF_CHECK(B.alloc(&d_wl, (int64_t)rp * n_rows));
+    KLNMF_CHECK(B.alloc(&d_fl, (int64_t)rp * n_cols));
+    KLNMF_CHECK(B.alloc(&d_ident, rp));
+    KLNMF_CHECK(cudaMemcpyAsync(d_ptr, col_ptr, sizeof(int64_t) * (n_cols + 1), cudaMemcpyHostToDevice, st));
+    if (nnz > 0) {
+        KLNMF_CHECK(cudaMemcpyAsync(d_row64, row_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+        KLNMF_CHECK(cudaMemcpyAsync(d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+        i64_to_i32<<<grid_for(nnz), 256, 0, st>>>(d_row64, nnz, d_idx);
+        KLNMF_CHECK_LAUNCH("i64_to_i32");
+    }
+    if (r * n_rows > 0) KLNMF_CHECK(cudaMemcpyAsync(d_w, w, sizeof(double) * r * n_rows, cudaMemcpyHostToDevice, st));
+    if (r * n_cols > 0) KLNMF_CHECK(cudaMemcpyAsync(d_f, f, sizeof(double) * r * n_cols, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_ident, ident.data(), sizeof(int32_t) * rp, cudaMemcpyHostToDevice, st));
+    int rc = klnmf_layout_to_device(d_w, r, n_rows, d_ident, rp, d_wl, 0, st);
+    if (rc) return rc;
+    rc = klnmf_layout_to_device(d_f, r, n_cols, d_ident, rp, d_fl, 0, st);
+    if (rc) return rc;
+    klnmf_side_t side;
+    side.ptr = d_ptr;
+    side.idx = d_idx;
+    side.val = d_val;
+    side.n_fix = n_rows;
+    side.n_mov = n_cols;
+    side.nnz = nnz;
+    return klnmf_kl_data_term_dev(&side, d_wl, d_fl, rp, d_ident, d_ident, (int32_t)r, 0, eps_div, out, st);
+}
+
+extern "C" int klnmf_row_sums(const double *factor, int64_t r, int64_t n, double *out) {
+    if (r < 0 || n < 0) return set_error_msg(1, "klnmf_row_sums: bad shape");
+    if (r == 0) return 0;
+    DevBufs B;
+    KLNMF_CHECK(cudaStreamCreateWithFlags(&B.st, cudaStreamNonBlocking));
+    cudaStream_t st = B.st;
+    double *d_fac, *d_out;
+    KLNMF_CHECK(B.alloc(&d_fac, r * n));
+    KLNMF_CHECK(B.alloc(&d_out, r));
+    if (r * n > 0) KLNMF_CHECK(cudaMemcpyAsync(d_fac, factor, sizeof(double) * r * n, cudaMemcpyHostToDevice, st));
+    int rc = row_sums_ref_layout(d_fac, r, n, d_out, st);
+    if (rc) return rc;
+    KLNMF_CHECK(cudaMemcpyAsync(out, d_out, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(cudaStreamSynchronize(st));
+    return 0;
+}

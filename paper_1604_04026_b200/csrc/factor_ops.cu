@@ -1,0 +1,207 @@
+// Factor-side device operations: layout conversion between the reference's
+// (r, n) fp64 layout and the device's item-major visit-order layout, the fp32
+// mode row sums (deterministic), factor statistics for the objective and
+// sparsity log, and the initial maintained products of the fp32 mode.
+//
+// Reference anchors: DenseFactor (sparse.py:168-206: row_sums :194-196,
+// sparsity :198-200), full_objective's regulariser sums (solver.py:229-233).
+#include "common.cuh"
+
+namespace klnmf {
+namespace {
+
+template <typename T>
+__global__ void to_device_kernel(const double *src, int64_t r, int64_t n, const int32_t *order,
+                                 int32_t rp, T *dst) {
+    // dst[i, tt] = src[order[tt], i]; padding columns = 0
+    const int64_t total = n * rp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / rp;
+        const int tt = (int)(e - i * rp);
+        dst[e] = tt < r ? (T)src[(int64_t)order[tt] * n + i] : (T)0;
+    }
+}
+
+template <typename T>
+__global__ void from_device_kernel(const T *src, int64_t r, int64_t n, const int32_t *order,
+                                   int32_t rp, double *dst) {
+    const int64_t total = n * r;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / r;
+        const int tt = (int)(e - i * r);
+        dst[(int64_t)order[tt] * n + i] = (double)src[i * rp + tt];
+    }
+}
+
+// fp32 row sums by position: each block sums a contiguous item range in fp64
+// (thread = position, items in order), then one pass adds block partials in
+// block order.  Fixed grid => deterministic and identical on every rank.
+constexpr int RS_BLOCKS = 1024;
+
+__global__ void row_sums_fast_partial(const float *fac, int64_t n_items, int32_t rp, double *partial) {
+    const int64_t per = (n_items + RS_BLOCKS - 1) / RS_BLOCKS;
+    const int64_t i0 = (int64_t)blockIdx.x * per;
+    const int64_t i1 = min(n_items, i0 + per);
+    for (int k = threadIdx.x; k < rp; k += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t i = i0;
+        for (; i + 3 < i1; i += 4) {
+            s0 += (double)__ldg(fac + i * rp + k);
+            s1 += (double)__ldg(fac + (i + 1) * rp + k);
+            s2 += (double)__ldg(fac + (i + 2) * rp + k);
+            s3 += (double)__ldg(fac + (i + 3) * rp + k);
+        }
+        for (; i < i1; ++i) s0 += (double)__ldg(fac + i * rp + k);
+        partial[(int64_t)blockIdx.x * rp + k] = (s0 + s1) + (s2 + s3);
+    }
+}
+
+__global__ void row_sums_fast_final(const double *partial, int32_t rp, int32_t r, double *out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= rp) return;
+    double s = 0.0;
+    if (k < r)
+        for (int b = 0; b < RS_BLOCKS; ++b) s += partial[(int64_t)b * rp + k];
+    out[k] = s;
+}
+
+// sum x^2, sum x, zero count over the r real columns (fixed grid, fixed tree)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) factor_stats_partial(const T *fac, int64_t n_items, int32_t rp,
+                                                           int32_t r, double *partial) {
+    __shared__ double sh[NT / 32];
+    const int64_t total = n_items * rp;
+    double s2 = 0.0, s1 = 0.0, zc = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * NT + threadIdx.x; e < total; e += (int64_t)gridDim.x * NT) {
+        const int tt = (int)(e % rp);
+        if (tt < r) {
+            const double x = (double)fac[e];
+            s2 += x * x;
+            s1 += x;
+            zc += (x == 0.0) ? 1.0 : 0.0;
+        }
+    }
+    const double a = block_sum_det<NT>(s2, sh);
+    const double b = block_sum_det<NT>(s1, sh);
+    const double c = block_sum_det<NT>(zc, sh);
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x * 3 + 0] = a;
+        partial[blockIdx.x * 3 + 1] = b;
+        partial[blockIdx.x * 3 + 2] = c;
+    }
+}
+
+__global__ void factor_stats_final(const double *partial, int nb, double *out) {
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s += partial[b * 3 + threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+// t[q] = sum_k fixed[i_q, pos_f(k)] * moving[j, pos_m(k)] in natural k order (fp64)
+template <int NT>
+__global__ void __launch_bounds__(NT) init_t_kernel(const int64_t *ptr, const int32_t *idx, int64_t n_mov,
+                                                    int64_t nnz, const float *fixed, const float *moving,
+                                                    int32_t rp, const int32_t *fpos, const int32_t *mpos,
+                                                    int32_t r, double *t) {
+    const int64_t q = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (q >= nnz) return;
+    int64_t lo = 0, hi = n_mov;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ptr[mid + 1] <= q) lo = mid + 1; else hi = mid;
+    }
+    const float *a = fixed + (int64_t)idx[q] * rp;
+    const float *b = moving + lo * rp;
+    double d = 0.0;
+    for (int k = 0; k < r; ++k) d = fma((double)__ldg(a + fpos[k]), (double)__ldg(b + mpos[k]), d);
+    t[q] = d;
+}
+
+inline unsigned grid_for(int64_t total, int nt) {
+    int64_t b = (total + nt - 1) / nt;
+    if (b < 1) b = 1;
+    if (b > 148 * 64) b = 148 * 64;
+    return (unsigned)b;
+}
+
+}  // namespace
+}  // namespace klnmf
+
+using namespace klnmf;
+
+extern "C" int klnmf_layout_to_device(const double *src, int64_t r, int64_t n, const int32_t *order,
+                                      int32_t rp, void *dst, int fp32, void *stream) {
+    const int64_t total = n * rp;
+    if (total == 0) return 0;
+    if (fp32)
+        to_device_kernel<float><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, r, n, order, rp,
+                                                                                    static_cast<float *>(dst));
+    else
+        to_device_kernel<double><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, r, n, order, rp,
+                                                                                     static_cast<double *>(dst));
+    KLNMF_CHECK_LAUNCH("to_device_kernel");
+    return 0;
+}
+
+extern "C" int klnmf_layout_from_device(const void *src, int64_t r, int64_t n, const int32_t *order,
+                                        int32_t rp, int fp32, double *dst, void *stream) {
+    const int64_t total = n * r;
+    if (total == 0) return 0;
+    if (fp32)
+        from_device_kernel<float><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+            static_cast<const float *>(src), r, n, order, rp, dst);
+    else
+        from_device_kernel<double><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+            static_cast<const double *>(src), r, n, order, rp, dst);
+    KLNMF_CHECK_LAUNCH("from_device_kernel");
+    return 0;
+}
+
+extern "C" int klnmf_row_sums_fast(const float *fac, int64_t n_items, int32_t rp, int32_t r,
+                                   double *out, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    double *partial = nullptr;
+    KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (size_t)RS_BLOCKS * (size_t)rp, st));
+    const int nt = rp < 128 ? ((rp + 31) / 32) * 32 : 128;
+    row_sums_fast_partial<<<RS_BLOCKS, nt, 0, st>>>(fac, n_items, rp, partial);
+    KLNMF_CHECK_LAUNCH("row_sums_fast_partial");
+    row_sums_fast_final<<<(rp + 127) / 128, 128, 0, st>>>(partial, rp, r, out);
+    KLNMF_CHECK_LAUNCH("row_sums_fast_final");
+    KLNMF_CHECK(cudaFreeAsync(partial, st));
+    return 0;
+}
+
+extern "C" int klnmf_factor_stats(const void *fac, int64_t n_items, int32_t rp, int32_t r, int fp32,
+                                  double *out_host, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    constexpr int NT = 256, NB = 512;
+    double *partial = nullptr;
+    KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (NB * 3 + 3), st));
+    if (fp32)
+        factor_stats_partial<float, NT><<<NB, NT, 0, st>>>(static_cast<const float *>(fac), n_items, rp, r, partial);
+    else
+        factor_stats_partial<double, NT><<<NB, NT, 0, st>>>(static_cast<const double *>(fac), n_items, rp, r, partial);
+    KLNMF_CHECK_LAUNCH("factor_stats_partial");
+    factor_stats_final<<<1, 32, 0, st>>>(partial, NB, partial + NB * 3);
+    KLNMF_CHECK_LAUNCH("factor_stats_final");
+    KLNMF_CHECK(cudaMemcpyAsync(out_host, partial + NB * 3, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(cudaFreeAsync(partial, st));
+    KLNMF_CHECK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+extern "C" int klnmf_init_t(const klnmf_side_t *side, const float *fixed, const float *moving, int32_t rp,
+                            const int32_t *fixed_pos, const int32_t *moving_pos, int32_t r, double *t,
+                            void *stream) {
+    constexpr int NT = 256;
+    if (side->nnz == 0) return 0;
+    const int64_t blocks = (side->nnz + NT - 1) / NT;
+    init_t_kernel<NT><<<(unsigned)blocks, NT, 0, as_stream(stream)>>>(side->ptr, side->idx, side->n_mov, side->nnz,
+                                                                      fixed, moving, rp, fixed_pos, moving_pos, r, t);
+    KLNMF_CHECK_LAUNCH("init_t_kernel");
+    return 0;
+}

@@ -1,0 +1,421 @@
+"""Device-resident plan: the B200 replacement of the reference's sweep loop.
+
+One ``DevicePlan`` owns, for its lifetime, every device buffer of a
+factorization (the ownership rule of SURVEY.md §8(b)): V in both
+orientations (CSC uploaded once, CSC of V^T built on the device by
+``klnmf_transpose``), the nnz buckets of each side's subproblems, both factors
+in the item-major visit-order layout, and (fp32 mode) the maintained
+products carried between half-steps.  ``half_step`` is the device version of
+``sweep`` (pkg/src/klnmf/solver.py:165-216): fixed-factor row sums
+(solver.py:288/294, sparse.py:194-196), then one launch per nnz bucket of the
+subproblem solver (_kernels.sweep_range, _kernels.py:123-144).
+
+Precision modes:
+  "fp64"  exact mode: fp64 storage, the reference's operation order, no FMA;
+          bit-identical to the reference (klnmf_solve_exact).
+  "fp32"  throughput mode: fp32 storage of V and the factors, fp64 arithmetic,
+          maintained products carried between half-steps (klnmf_solve_fast).
+
+Multi-GPU (torch.distributed, one process per GPU): every rank holds V and
+both factors in full; subproblems are split into contiguous nnz-balanced
+ranges (columns for the F-update, rows for the W-update); after each
+half-step the updated factor rows (and, in fp32 mode, the maintained
+products of the updated entries) are all-gathered.  Results are bitwise
+independent of the rank count: each subproblem is solved by exactly one rank
+with identical inputs, and row sums are computed from the full replica.
+
+torch is used here only as plumbing: device allocation, the current stream,
+and NCCL collectives.  All arithmetic runs in libklnmf.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _lib
+from .subproblem import SolveStats, Tolerances
+
+INT64_MAX = np.iinfo(np.int64).max
+
+
+def round_rp(r: int) -> int:
+    return (r + 3) // 4 * 4
+
+
+def nnz_balanced_ranges(ptr: np.ndarray, parts: int):
+    """Contiguous item ranges [lo, hi) with about equal nnz (atomic items)."""
+    ptr = np.asarray(ptr, dtype=np.int64)
+    n = ptr.shape[0] - 1
+    nnz = int(ptr[-1])
+    bounds = [0]
+    for q in range(1, parts):
+        target = (nnz * q) // parts
+        b = int(np.searchsorted(ptr, target, side="left"))
+        b = min(max(b, bounds[-1]), n)
+        bounds.append(b)
+    bounds.append(n)
+    return [(bounds[q], bounds[q + 1]) for q in range(parts)]
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+@dataclasses.dataclass
+class SidePlan:
+    name: str                 # "F" (columns of V) or "W" (rows of V)
+    ptr: torch.Tensor         # int64[n_mov+1]
+    idx: torch.Tensor         # int32[nnz]
+    val: torch.Tensor         # float32/64[nnz]
+    n_fix: int
+    n_mov: int
+    nnz: int
+    ptr_host: np.ndarray
+    ranges: list              # per-rank [lo, hi)
+    items: torch.Tensor       # int32, this rank's items, sorted by nnz descending
+    buckets: list             # [(kernel_id, start, count)], largest first
+    tmap: torch.Tensor | None = None  # int32[nnz] entry -> position in the other side
+
+    def side_struct(self) -> _lib.Side:
+        return _lib.Side(self.ptr.data_ptr(), self.idx.data_ptr(), self.val.data_ptr(),
+                         self.n_fix, self.n_mov, self.nnz)
+
+
+class DevicePlan:
+    def __init__(self, V, rank: int, precision: str = "fp64", device=None, group=None,
+                 ledger=None, fast_kernels: list | None = None):
+        if precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+        if not torch.cuda.is_available():
+            raise RuntimeError("DevicePlan needs a CUDA device (no CPU fallback)")
+        _lib.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.fp32 = precision == "fp32"
+        self.precision = precision
+        self.vdt = torch.float32 if self.fp32 else torch.float64
+        self.r = int(rank)
+        self.rp = round_rp(self.r)
+        self.n, self.m = V.shape
+        self.nnz = V.nnz
+        if self.nnz >= 2**31 - 1:
+            raise ValueError("nnz must be < 2^31")
+        self.group = group
+        if group is not None:
+            import torch.distributed as dist
+            self.rank_id = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+        else:
+            self.rank_id, self.world = 0, 1
+        self.ledger = ledger
+        dev = self.dev
+
+        with torch.cuda.device(dev):
+            self.stream_ptr = torch.cuda.current_stream(dev).cuda_stream
+            # CSC of V (F-side) uploaded once; CSC of V^T (W-side) built on device
+            csc_ptr = torch.from_numpy(V.col_ptr).to(dev)
+            csc_idx = torch.from_numpy(V.row_idx).to(dev).to(torch.int32)
+            csc_val = torch.from_numpy(V.values).to(dev).to(self.vdt)
+            csr_ptr = torch.empty(self.n + 1, dtype=torch.int64, device=dev)
+            csr_idx = torch.empty(self.nnz, dtype=torch.int32, device=dev)
+            csr_val = torch.empty(self.nnz, dtype=self.vdt, device=dev)
+            map_csr2csc = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            map_csc2csr = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            _lib.call("klnmf_transpose", csc_ptr.data_ptr(), csc_idx.data_ptr(), csc_val.data_ptr(),
+                      csc_val.element_size(), self.n, self.m, self.nnz, csr_ptr.data_ptr(),
+                      csr_idx.data_ptr(), csr_val.data_ptr(), map_csr2csc.data_ptr(),
+                      map_csc2csr.data_ptr(), self.stream_ptr)
+            csr_ptr_host = csr_ptr.cpu().numpy()
+
+            self.fast_kernels = fast_kernels if fast_kernels is not None else _lib.fast_kernels()
+            self.sides = {
+                "F": self._make_side("F", csc_ptr, csc_idx, csc_val, self.n, self.m, V.col_ptr,
+                                     map_csc2csr if self.fp32 else None),
+                "W": self._make_side("W", csr_ptr, csr_idx, csr_val, self.m, self.n, csr_ptr_host,
+                                     map_csr2csc if self.fp32 else None),
+            }
+            self._track("V_csc", csc_ptr, csc_idx, csc_val)
+            self._track("V_csr", csr_ptr, csr_idx, csr_val)
+            if self.fp32:
+                self._track("entry_maps", map_csr2csc, map_csc2csr)
+            self.factors = {
+                "W": torch.zeros(self.n, self.rp, dtype=self.vdt, device=dev),
+                "F": torch.zeros(self.m, self.rp, dtype=self.vdt, device=dev),
+            }
+            self._track("W", self.factors["W"])
+            self._track("F", self.factors["F"])
+            self.order = {"W": None, "F": None}  # natural coordinate at each position
+            nz = max(self.nnz, 1)
+            if self.fp32:
+                self.t = {"csc": torch.zeros(nz, dtype=torch.float64, device=dev),
+                          "csr": torch.zeros(nz, dtype=torch.float64, device=dev)}
+                self._track("t", self.t["csc"], self.t["csr"])
+                need_stream = any(b[0] == self._stream_kernel_id() and b[2] > 0
+                                  for s in self.sides.values() for b in s.buckets)
+                self.scratch = torch.empty(2 * nz if need_stream else 1, dtype=torch.float64, device=dev)
+            else:
+                self.t = None
+                self.scratch = torch.empty(nz, dtype=torch.float64, device=dev)
+            self._track("scratch", self.scratch)
+            self.t_current = None  # which maintained-product array is valid ("csc"/"csr")
+            self.stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
+            self.sum_pos = torch.zeros(self.rp, dtype=torch.float64, device=dev)
+            self._perm = torch.zeros(3, self.rp, dtype=torch.int32, device=dev)
+            self._pos = torch.zeros(2, self.rp, dtype=torch.int32, device=dev)
+
+    # ------------------------------------------------------------------
+    def _track(self, name, *tensors):
+        if self.ledger is not None:
+            self.ledger.track(f"dev_{name}", *tensors)
+
+    def _stream_kernel_id(self) -> int:
+        for kid, cap, _, _ in self.fast_kernels:
+            if cap < 0:
+                return kid
+        return -1
+
+    def _make_side(self, name, ptr, idx, val, n_fix, n_mov, ptr_host, tmap) -> SidePlan:
+        ranges = nnz_balanced_ranges(ptr_host, self.world)
+        lo, hi = ranges[self.rank_id]
+        if self.fp32:
+            caps = [c for _, c, _, _ in self.fast_kernels]
+            bounds = np.array([c if c >= 0 else INT64_MAX for c in caps], dtype=np.int64)
+            kids = [k for k, _, _, _ in self.fast_kernels]
+        else:
+            bounds = np.array([INT64_MAX], dtype=np.int64)
+            kids = [-1]
+        items = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=self.dev)
+        counts = np.zeros(len(bounds), dtype=np.int64)
+        _lib.call("klnmf_bucketize", ptr.data_ptr(), lo, hi, bounds.ctypes.data, len(bounds),
+                  items.data_ptr(), counts.ctypes.data, self.stream_ptr)
+        # items are sorted by nnz descending: the largest bucket comes first
+        buckets = []
+        start = 0
+        for b in range(len(bounds) - 1, -1, -1):
+            c = int(counts[b])
+            buckets.append((kids[b], start, c))
+            start += c
+        assert start == hi - lo, (start, hi, lo)
+        return SidePlan(name, ptr, idx, val, int(n_fix), int(n_mov), int(ptr[-1].item()) if n_mov else 0,
+                        np.asarray(ptr_host, dtype=np.int64), ranges, items, buckets, tmap)
+
+    def _h2d_i32(self, dst: torch.Tensor, arr) -> None:
+        host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32))
+        dst.copy_(host, non_blocking=False)
+
+    def _padded(self, perm: np.ndarray) -> np.ndarray:
+        out = np.arange(self.rp, dtype=np.int32)
+        out[: self.r] = perm
+        return out
+
+    # ------------------------------------------------------------------
+    def set_factors(self, w: np.ndarray, f: np.ndarray, order: np.ndarray | None = None) -> None:
+        """Upload (r, n) / (r, m) fp64 factors, stored in visit order `order`."""
+        order = np.arange(self.r) if order is None else np.asarray(order)
+        for name, arr, n_items in (("W", w, self.n), ("F", f, self.m)):
+            arr = np.ascontiguousarray(arr, dtype=np.float64)
+            if arr.shape != (self.r, n_items):
+                raise ValueError(f"{name} must have shape {(self.r, n_items)}")
+            src = torch.from_numpy(arr).to(self.dev)
+            o = torch.from_numpy(self._padded(order)).to(self.dev)
+            _lib.call("klnmf_layout_to_device", src.data_ptr(), self.r, n_items, o.data_ptr(), self.rp,
+                      self.factors[name].data_ptr(), int(self.fp32), self.stream_ptr)
+            self.order[name] = np.asarray(order, dtype=np.int64).copy()
+        self.t_current = None
+
+    def get_factors(self):
+        """Download both factors as (r, n) / (r, m) fp64 numpy arrays."""
+        out = []
+        for name, n_items in (("W", self.n), ("F", self.m)):
+            dst = torch.empty(self.r, n_items, dtype=torch.float64, device=self.dev)
+            o = torch.from_numpy(self._padded(self.order[name])).to(self.dev)
+            _lib.call("klnmf_layout_from_device", self.factors[name].data_ptr(), self.r, n_items, o.data_ptr(),
+                      self.rp, int(self.fp32), dst.data_ptr(), self.stream_ptr)
+            out.append(dst.cpu().numpy())
+        return out[0], out[1]
+
+    # ------------------------------------------------------------------
+    def row_sums_pos(self, name: str, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Row sums of a factor by storage position (fp64, device)."""
+        out = self.sum_pos if out is None else out
+        fac = self.factors[name]
+        n_items = fac.shape[0]
+        fn = "klnmf_row_sums_fast" if self.fp32 else "klnmf_row_sums_exact"
+        _lib.call(fn, fac.data_ptr(), n_items, self.rp, self.r, out.data_ptr(), self.stream_ptr)
+        return out
+
+    def row_sums_natural(self, name: str) -> np.ndarray:
+        pos = self.row_sums_pos(name, torch.zeros(self.rp, dtype=torch.float64, device=self.dev))
+        pos = pos.cpu().numpy()[: self.r]
+        out = np.empty(self.r)
+        out[self.order[name]] = pos
+        return out
+
+    def _init_t(self, which: str) -> None:
+        """t at every entry of one orientation = <W_i, F_j> from the stored factors."""
+        side = self.sides["W"] if which == "csr" else self.sides["F"]
+        fixed = self.factors["F"] if which == "csr" else self.factors["W"]
+        moving = self.factors["W"] if which == "csr" else self.factors["F"]
+        fo = self.order["F"] if which == "csr" else self.order["W"]
+        mo = self.order["W"] if which == "csr" else self.order["F"]
+        self._h2d_i32(self._pos[0], self._padded(np.argsort(fo)))
+        self._h2d_i32(self._pos[1], self._padded(np.argsort(mo)))
+        s = side.side_struct()
+        _lib.call("klnmf_init_t", ctypes.byref(s), fixed.data_ptr(), moving.data_ptr(), self.rp,
+                  self._pos[0].data_ptr(), self._pos[1].data_ptr(), self.r, self.t[which].data_ptr(),
+                  self.stream_ptr)
+        self.t_current = which
+
+    def half_step(self, which: str, ids, ids_next=None, alpha: float = 0.0, beta: float = 0.0,
+                  tol: Tolerances = Tolerances(), sums_pos: np.ndarray | None = None) -> None:
+        """Solve every subproblem of one side (which="F": columns, W fixed;
+        which="W": rows, F fixed) in place, visiting coordinates in `ids`.
+
+        The moving factor is re-stored in visit order `ids` (F) or `ids_next`
+        (W, the next iteration's order; defaults to `ids`).  `sums_pos`
+        overrides the device row sums (the public sweep() passes the
+        caller's sums, solver.py:165).
+        """
+        ids = np.asarray(ids, dtype=np.int64)
+        fixed_name = "W" if which == "F" else "F"
+        side = self.sides[which]
+        if self.order[fixed_name] is None or not np.array_equal(self.order[fixed_name], ids):
+            raise RuntimeError(f"fixed factor {fixed_name} is not stored in the visit order")
+        o_mov = self.order[which]
+        out_order = ids if (which == "F" or ids_next is None) else np.asarray(ids_next, dtype=np.int64)
+        perm_in = np.argsort(o_mov)[ids]
+        perm_out = np.argsort(out_order)[ids]
+        nat_pos = np.argsort(ids)
+        host = np.stack([self._padded(perm_in), self._padded(perm_out), self._padded(nat_pos)])
+        self._perm.copy_(torch.from_numpy(host))
+        if sums_pos is None:
+            self.row_sums_pos(fixed_name)
+        else:
+            sp = np.zeros(self.rp)
+            sp[: self.r] = np.asarray(sums_pos, dtype=np.float64)
+            self.sum_pos.copy_(torch.from_numpy(sp))
+
+        a = _lib.SolveArgs()
+        a.side = side.side_struct()
+        a.fixed = self.factors[fixed_name].data_ptr()
+        a.moving = self.factors[which].data_ptr()
+        a.sum_pos = self.sum_pos.data_ptr()
+        a.perm_in = self._perm[0].data_ptr()
+        a.perm_out = self._perm[1].data_ptr()
+        a.nat_pos = self._perm[2].data_ptr()
+        a.r, a.rp = self.r, self.rp
+        a.alpha, a.beta = float(alpha), float(beta)
+        a.eps_grad, a.eps_x, a.eps_div = float(tol.eps_grad), float(tol.eps_x), float(tol.eps_div)
+        a.inner_cap = int(tol.inner_iter_cap)
+        a.stats = self.stats.data_ptr()
+        a.scratch = self.scratch.data_ptr()
+        item_base = side.items.data_ptr()
+        if self.fp32:
+            need = "csr" if which == "F" else "csc"
+            if self.t_current != need:
+                self._init_t(need)
+            a.tmap = side.tmap.data_ptr()
+            a.t_in = self.t[need].data_ptr()
+            a.t_out = self.t["csc" if which == "F" else "csr"].data_ptr()
+            for kid, start, count in side.buckets:
+                if count == 0:
+                    continue
+                a.items = item_base + 4 * start
+                a.n_items = count
+                _lib.check(_lib.load().klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr),
+                           "klnmf_solve_fast")
+            self.t_current = "csc" if which == "F" else "csr"
+        else:
+            for _, start, count in side.buckets:
+                if count == 0:
+                    continue
+                a.items = item_base + 4 * start
+                a.n_items = count
+                _lib.check(_lib.load().klnmf_solve_exact(ctypes.byref(a), self.stream_ptr),
+                           "klnmf_solve_exact")
+        self.order[which] = np.asarray(out_order, dtype=np.int64).copy()
+        if self.world > 1:
+            self._exchange(which)
+
+    def _exchange(self, which: str) -> None:
+        """All-gather the updated rows of the moving factor (and, in fp32
+        mode, the maintained products of the updated entries)."""
+        side = self.sides[which]
+        allgather_ranges(self.factors[which], side.ranges, self.group)
+        if self.fp32:
+            eranges = [(int(side.ptr_host[lo]), int(side.ptr_host[hi])) for lo, hi in side.ranges]
+            allgather_ranges(self.t["csc" if which == "F" else "csr"], eranges, self.group)
+
+    # ------------------------------------------------------------------
+    def take_stats(self) -> SolveStats:
+        """Read and reset the device counters."""
+        arr = self.stats.cpu().numpy()
+        self.stats.zero_()
+        if self.world > 1:
+            # every rank counted only its own subproblems
+            import torch.distributed as dist
+            t = torch.from_numpy(arr.copy()).to(self.dev)
+            dist.all_reduce(t, group=self.group)
+            arr = t.cpu().numpy()
+        return SolveStats.from_array(arr)
+
+    def objective(self, alpha1=0.0, alpha2=0.0, beta1=0.0, beta2=0.0, eps_div=1e-16):
+        """(kl, total, sparsity_w, sparsity_f) -- full_objective, solver.py:219-234."""
+        side = self.sides["F"]
+        s = side.side_struct()
+        wpos = self._padded(np.argsort(self.order["W"]))
+        fpos = self._padded(np.argsort(self.order["F"]))
+        self._h2d_i32(self._pos[0], wpos)
+        self._h2d_i32(self._pos[1], fpos)
+        data = ctypes.c_double()
+        _lib.call("klnmf_kl_data_term_dev", ctypes.byref(s), self.factors["W"].data_ptr(),
+                  self.factors["F"].data_ptr(), self.rp, self._pos[0].data_ptr(), self._pos[1].data_ptr(),
+                  self.r, int(self.fp32), float(eps_div), ctypes.byref(data), self.stream_ptr)
+        kl = float(data.value) + float(self.row_sums_natural("W") @ self.row_sums_natural("F"))
+        st = {}
+        for name in ("W", "F"):
+            out = (ctypes.c_double * 3)()
+            fac = self.factors[name]
+            _lib.call("klnmf_factor_stats", fac.data_ptr(), fac.shape[0], self.rp, self.r, int(self.fp32),
+                      out, self.stream_ptr)
+            st[name] = (out[0], out[1], out[2])
+        total = kl
+        total += 0.5 * alpha1 * st["W"][0]
+        total += 0.5 * alpha2 * st["F"][0]
+        total += beta1 * st["W"][1]
+        total += beta2 * st["F"][1]
+        spw = st["W"][2] / (self.r * self.n)
+        spf = st["F"][2] / (self.r * self.m)
+        return kl, total, spw, spf
+
+    def synchronize(self) -> None:
+        torch.cuda.synchronize(self.dev)
+
+
+def allgather_ranges(buf: torch.Tensor, ranges, group) -> None:
+    """In-place all-gather of uneven contiguous first-axis ranges of `buf`.
+
+    Rank q owns rows ranges[q] = (lo, hi); afterwards every rank holds all
+    rows.  Padded to the longest range for one all_gather_into_tensor.
+    """
+    import torch.distributed as dist
+
+    me = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    maxlen = max(hi - lo for lo, hi in ranges)
+    if maxlen == 0:
+        return
+    tail = tuple(buf.shape[1:])
+    send = torch.zeros((maxlen,) + tail, dtype=buf.dtype, device=buf.device)
+    lo, hi = ranges[me]
+    send[: hi - lo] = buf[lo:hi]
+    recv = torch.empty((world * maxlen,) + tail, dtype=buf.dtype, device=buf.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    for q, (lo, hi) in enumerate(ranges):
+        if q != me and hi > lo:
+            buf[lo:hi] = recv[q * maxlen: q * maxlen + (hi - lo)]
