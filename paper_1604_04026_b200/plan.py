@@ -271,15 +271,22 @@ class DevicePlan:
                   self.stream_ptr)
         self.t_current = which
 
+    # kernels launched per outer iteration besides the solver buckets:
+    # the fast row sums are two launches per half-step
+    aux_launches_per_step = 4
+
     def half_step(self, which: str, ids, ids_next=None, alpha: float = 0.0, beta: float = 0.0,
-                  tol: Tolerances = Tolerances(), sums_pos: np.ndarray | None = None) -> None:
+                  tol: Tolerances = Tolerances(), sums_pos: np.ndarray | None = None,
+                  events: list | None = None) -> None:
         """Solve every subproblem of one side (which="F": columns, W fixed;
         which="W": rows, F fixed) in place, visiting coordinates in `ids`.
 
         The moving factor is re-stored in visit order `ids` (F) or `ids_next`
         (W, the next iteration's order; defaults to `ids`).  `sums_pos`
         overrides the device row sums (the public sweep() passes the
-        caller's sums, solver.py:165).
+        caller's sums, solver.py:165).  With `events` (a list), a CUDA event
+        pair is recorded around every solver launch and appended as
+        (which, kernel_id, start, end).
         """
         ids = np.asarray(ids, dtype=np.int64)
         fixed_name = "W" if which == "F" else "F"
@@ -327,8 +334,12 @@ class DevicePlan:
                     continue
                 a.items = item_base + 4 * start
                 a.n_items = count
+                ev = self._event_pair(events)
                 _lib.check(_lib.load().klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr),
                            "klnmf_solve_fast")
+                if ev is not None:
+                    ev[1].record(torch.cuda.current_stream(self.dev))
+                    events.append((which, kid, ev[0], ev[1]))
             self.t_current = "csc" if which == "F" else "csr"
         else:
             for _, start, count in side.buckets:
@@ -336,11 +347,23 @@ class DevicePlan:
                     continue
                 a.items = item_base + 4 * start
                 a.n_items = count
+                ev = self._event_pair(events)
                 _lib.check(_lib.load().klnmf_solve_exact(ctypes.byref(a), self.stream_ptr),
                            "klnmf_solve_exact")
+                if ev is not None:
+                    ev[1].record(torch.cuda.current_stream(self.dev))
+                    events.append((which, -1, ev[0], ev[1]))
         self.order[which] = np.asarray(out_order, dtype=np.int64).copy()
         if self.world > 1:
             self._exchange(which)
+
+    def _event_pair(self, events):
+        if events is None:
+            return None
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream(self.dev))
+        return e0, e1
 
     def _exchange(self, which: str) -> None:
         """All-gather the updated rows of the moving factor (and, in fp32
