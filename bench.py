@@ -46,13 +46,16 @@ def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-baseline sample budget")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-kernel-events", action="store_true")
     return ap.parse_args()
 
 
@@ -92,6 +95,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if self.index < 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
@@ -296,12 +301,14 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
+    plan.take_stats()
     step_ms = []
     per_step_events = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(-1 if args.no_clocks else local) as clocks:
         for _ in range(args.steps):
-            flush.zero_()
-            ev = []
+            if not args.no_flush:
+                flush.zero_()
+            ev = None if args.no_kernel_events else []
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -311,10 +318,11 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
     for e0, e1, ev in per_step_events:
         step_ms.append(e0.elapsed_time(e1))
-        for (side, kid, a, b) in ev:
+        for (side, kid, a, b) in ev or []:
             kernel_ms.setdefault((side, kid), []).append(a.elapsed_time(b))
             launch_count[0] += 1
     launch_count[0] += plan.aux_launches_per_step * args.steps
+    st = plan.take_stats()
     total_ms = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -327,15 +335,17 @@ def run_ours(args):
 
     # dominant kernel and its roofline
     peak, peak_kind = peaks()
+    if not kernel_ms:
+        kernel_ms[("F", -2)] = [0.0]
     dom = max(kernel_ms.items(), key=lambda kv: np.sum(kv[1]))
     (dside, dkid), dms = dom
     sp = plan.sides[dside]
-    start, count = next((s, c) for k, s, c in sp.buckets if k == dkid)
+    start, count = next(((s, c) for k, s, c in sp.buckets if k == dkid), (0, 0))
     items = sp.items[start:start + count].cpu().numpy()
     dbytes = algorithmic_bytes(sp.ptr_host, items, r)
     avg_s = float(np.mean(dms)) * 1e-3
-    achieved = dbytes / avg_s / 1e9
-    kinfo = next(k for k in plan.fast_kernels if k[0] == dkid)
+    achieved = dbytes / avg_s / 1e9 if avg_s > 0 else 0.0
+    kinfo = next((k for k in plan.fast_kernels if k[0] == dkid), (dkid, 0, 0, 0))
     traffic = None
     prof = REPO / "profiles" / "traffic.json"
     if prof.exists():
@@ -374,6 +384,10 @@ def run_ours(args):
                          "step_frac": it_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
                          "step_algorithmic_bytes": it_bytes},
             "kernels": kernel_table,
+            "solver_stats_per_step": {"newton_steps": st.inner_iters / args.steps,
+                                      "newton_steps_per_visit": st.inner_iters / args.steps
+                                      / ((spec.n + spec.m) * r),
+                                      "cap_hits": st.cap_hits, "degenerate": st.degenerate},
             "gpu_launches": launch_count[0],
             "clocks": clocks.summary(),
         }
