@@ -163,13 +163,21 @@ def _check(mov_gpu, mov_or, t_gpu, t_or, label):
     assert np.mean(trel > 1e-4) < 1e-3
 
 
-@pytest.mark.parametrize("name", ["C2", "C3"])
+def _check_stats(sg, so):
+    """Newton-step counts follow the same control flow as the oracle (allow a
+    handful of flips from fp32 rounding-boundary differences)."""
+    assert sg.passes == so[3]
+    assert sg.cap_hits <= so[0] + 2 and sg.degenerate == so[1]
+    assert abs(sg.inner_iters - so[2]) <= max(3, 1e-4 * so[2]), (sg, so)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
 def test_half_step_vs_fp32_oracle(cuda_ok, name):
     from paper_1604_04026_b200 import synth
     from paper_1604_04026_b200.plan import DevicePlan
 
     spec = _spec(name)
-    if name == "C3":
+    if name in ("C3", "C4"):
         spec = spec.scaled(m=8000)  # keeps the oracle step to seconds
     V = synth.generate(spec)
     w0, f0 = synth.initial_factors(spec)
@@ -179,7 +187,7 @@ def test_half_step_vs_fp32_oracle(cuda_ok, name):
     for which, a, b in (("F", spec.reg.alpha2, spec.reg.beta2), ("W", spec.reg.alpha1, spec.reg.beta1)):
         mg, mo, tg, to, sg, so = _compare_half_step(plan, which, ids, a, b)
         _check(mg, mo, tg, to, f"{name} {which}")
-        assert sg.passes == so[3]
+        _check_stats(sg, so)
 
 
 def test_every_bucket_kernel(cuda_ok):
@@ -214,6 +222,7 @@ def test_every_bucket_kernel(cuda_ok):
     for alpha, beta in ((0.0, 0.0), (0.05, 0.1)):
         mg, mo, tg, to, sg, so = _compare_half_step(plan, "F", ids, alpha, beta)
         _check(mg, mo, tg, to, f"buckets F a={alpha} b={beta}")
+        _check_stats(sg, so)
         assert sg.passes == len(sizes)
 
 
@@ -237,3 +246,59 @@ def test_device_transpose_and_buckets(cuda_ok):
         sz = np.diff(s.ptr_host)[items]
         assert np.all(np.diff(sz) <= 0)  # largest first
         assert sorted(items.tolist()) == list(range(s.n_mov))
+
+
+@pytest.mark.parametrize("name,m", [("C3", None), ("C4", 20000)])
+def test_fp32_iterations_per_half_step(cuda_ok, name, m):
+    """Five outer iterations through the plan -- visit order changing every
+    iteration, the W-sweep writing the next iteration's order, maintained
+    products carried both ways -- with every half-step compared against the
+    fp32-mode restatement from the same state (then reset to it, so chaotic
+    growth of rounding flips cannot mask or fake a kernel bug).  Exercises the
+    late-iteration regime (sparse factors, few moves) where batched gradients
+    are reused across coordinates; full C3 includes the long-row kernel."""
+    import torch
+
+    from paper_1604_04026_b200 import synth
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    spec = _spec(name)
+    if m is not None:
+        spec = spec.scaled(m=m)
+    V = synth.generate(spec)
+    w0, f0 = synth.initial_factors(spec)
+    r, rp, reg = spec.rank, (spec.rank + 3) // 4 * 4, spec.reg
+    plan = DevicePlan(V, r, "fp32")
+    rng = np.random.default_rng(spec.seed)
+    ids = rng.permutation(r)
+    plan.set_factors(w0, f0, order=ids)
+    for it in range(5):
+        nxt = rng.permutation(r)
+        for which, a, b in (("F", reg.alpha2, reg.beta2), ("W", reg.alpha1, reg.beta1)):
+            side = plan.sides[which]
+            fixed_name = "W" if which == "F" else "F"
+            need = "csr" if which == "F" else "csc"
+            if plan.t_current != need:
+                plan._init_t(need)
+            t0 = plan.t[need].cpu().numpy()[side.tmap.cpu().numpy()]
+            fixed = plan.factors[fixed_name].cpu().numpy()
+            mov = plan.factors[which].cpu().numpy()
+            mov_vis = np.zeros_like(mov)
+            mov_vis[:, :r] = mov[:, np.argsort(plan.order[which])[ids]]
+            sums = plan.row_sums_pos(fixed_name, torch.zeros(rp, dtype=torch.float64, device=plan.dev))
+            mo, to = mov_vis.copy(), t0.copy()
+            so = oracle.sweep_fp32(side.ptr.cpu().numpy(), side.idx.cpu().numpy(), side.val.cpu().numpy(), fixed,
+                                   rp, r, sums.cpu().numpy(), mo, to, None, a, b)
+            out_order = ids if which == "F" else nxt
+            plan.half_step(which, ids, nxt if which == "W" else None, alpha=a, beta=b)
+            sg = plan.take_stats()
+            got = plan.factors[which].cpu().numpy()
+            got_vis = got[:, np.argsort(out_order)[ids]]
+            tg = plan.t["csc" if which == "F" else "csr"].cpu().numpy()[: plan.nnz]
+            _check(got_vis, mo[:, :r], tg, to, f"{name} it{it + 1} {which}")
+            _check_stats(sg, so)
+            reset = np.zeros_like(got)
+            reset[:, np.argsort(out_order)[ids]] = mo[:, :r]
+            plan.factors[which].copy_(torch.from_numpy(reset))
+            plan.t["csc" if which == "F" else "csr"][: plan.nnz].copy_(torch.from_numpy(to))
+        ids = nxt
