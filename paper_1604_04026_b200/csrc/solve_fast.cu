@@ -31,7 +31,9 @@
 //   solve_block_kernel<NT, NPL> one subproblem per block (NT threads).
 //   solve_stream_kernel<NT>     any size, one block per subproblem, per-entry
 //       state in global memory (long rows of the W side).
+#include <cooperative_groups.h>
 #include <cstdio>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -41,6 +43,28 @@ namespace {
 constexpr int C = 4;       // coordinates per batch (16 B of fp32 per entry)
 constexpr int NV = 2 * C;  // reduced values per pass: g partials then h partials
 constexpr int STAGES = 3;  // cp.async ring depth
+constexpr int KMAX_RP = 256;  // largest padded rank of the fp32 kernels (row sums staged in smem)
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [I0, N).
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N>(f);
+    }
+}
+
+// Adds one entry's contribution to a coordinate's (g, h) partial sums.
+// The reference skips a == 0 (_kernels.py:32).  With eps_div > 0, u and z are
+// finite, so an a == 0 term adds exactly +0.0 and the (if-converted, select-
+// heavy) guard is dropped; GUARD keeps it for eps_div == 0, where u may be inf.
+template <bool GUARD>
+__device__ __forceinline__ void accum(double &g, double &h, double u, double z, double av) {
+    if (!GUARD || av != 0.0) {
+        g = fma(u, av, g);
+        h = fma(z * av, av, h);
+    }
+}
 
 struct Counters {
     unsigned n_inner = 0, n_cap = 0, n_deg = 0;
@@ -88,12 +112,24 @@ __device__ __forceinline__ double newton_step(double g, double h, double &x, int
     return delta;
 }
 
+// 1/x: MUFU approximation refined by two Newton steps (<= 1 ulp); x == 0
+// (only possible with eps_div == 0) returns inf like the IEEE division.
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    return x == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : r;
+}
+
 __device__ __forceinline__ void entry_update(double delta, double av, float v, double eps, double &t, double &u,
                                              double &z) {
     double tn = fma(delta, av, t);
     if (tn < 0.0) tn = 0.0;
     t = tn;
-    const double ri = 1.0 / (tn + eps);
+    const double ri = fast_rcp(tn + eps);
     u = (double)v * ri;
     z = u * ri;
 }
@@ -179,6 +215,9 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     float *xo = xs + rps;
     const int64_t slot = (int64_t)blockIdx.x * GPB + grp;
     const bool valid = slot < a.n_items;
+    __shared__ double ssum[KMAX_RP];  // fixed-factor row sums by position
+    for (int k = tid; k < r; k += NT) ssum[k] = a.sum_pos[k];
+    __syncthreads();
     if (!__any_sync(FULL_MASK, valid)) return;
 
     const float *fixed = static_cast<const float *>(a.fixed);
@@ -202,7 +241,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
             v[e] = val[q];
             const double tq = a.t_in[a.tmap ? (int64_t)a.tmap[q] : q];
             t[e] = tq;
-            const double ri = 1.0 / (tq + a.eps_div);
+            const double ri = fast_rcp(tq + a.eps_div);
             u[e] = (double)v[e] * ri;
             z[e] = u[e] * ri;
         } else {
@@ -247,33 +286,32 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
 
         double red[NV];
         bool fresh = false;  // partials valid for the current t
-#pragma unroll
-        for (int cc = 0; cc < C; ++cc) {
+        static_for<0, C>([&](auto cc_c) {  // compile-time coordinate index
+            constexpr int cc = decltype(cc_c)::value;
             const int tt = ch * C + cc;
-            if (tt >= r) break;  // uniform
+            if (tt >= r) return;
             if (__any_sync(FULL_MASK, !fresh)) {
                 // pass: partial sums of coordinates cc..C-1 on the current t
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
+                auto pass = [&](auto guard) {
 #pragma unroll
-                for (int e = 0; e < NPL; ++e) {
-                    const float4 a4 = Ach[e * NT];
+                    for (int e = 0; e < NPL; ++e) {
+                        const float4 a4 = Ach[e * NT];
 #pragma unroll
-                    for (int q = cc; q < C; ++q) {
-                        const double av = (double)f4_get(a4, q);
-                        if (av != 0.0) {
-                            red[q] = fma(u[e], av, red[q]);
-                            red[C + q] = fma(z[e] * av, av, red[C + q]);
-                        }
+                        for (int q = cc; q < C; ++q)
+                            accum<decltype(guard)::value>(red[q], red[C + q], u[e], z[e], (double)f4_get(a4, q));
                     }
-                }
+                };
+                if (eps > 0.0) pass(std::false_type{});
+                else pass(std::true_type{});
                 TReduce<L>::run(red, gl);
                 fresh = true;
             }
             const double gp = fetch<L>(red, cc);
             const double hp = fetch<L>(red, C + cc);
             double x = (double)xs[tt];
-            const double base = a.sum_pos[tt];
+            const double base = ssum[tt];
             double g = (base + alpha * x + a.beta) - gp;
             double h = alpha + hp;
             int inner = 0;
@@ -315,7 +353,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
             }
             if (moved) fresh = false;
             if (gl == 0 && valid) xo[tt] = (float)x;
-        }
+        });
     }
     cp_wait<0>();
     __syncwarp();
@@ -409,6 +447,8 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     const int64_t lo = a.side.ptr[j];
     const int s = (int)(a.side.ptr[j + 1] - lo);
 
+    __shared__ double ssum[KMAX_RP];
+    for (int k = tid; k < r; k += NT) ssum[k] = a.sum_pos[k];
     for (int k = tid; k < r; k += NT) xs[k] = moving[j * rp + a.perm_in[k]];
 
     double t[NPL], u[NPL], z[NPL];
@@ -423,7 +463,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
             v[e] = val[q];
             const double tq = a.t_in[a.tmap ? (int64_t)a.tmap[q] : q];
             t[e] = tq;
-            const double ri = 1.0 / (tq + a.eps_div);
+            const double ri = fast_rcp(tq + a.eps_div);
             u[e] = (double)v[e] * ri;
             z[e] = u[e] * ri;
         } else {
@@ -466,30 +506,29 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 
         double red[NV];
         bool fresh = false;
-#pragma unroll
-        for (int cc = 0; cc < C; ++cc) {
+        static_for<0, C>([&](auto cc_c) {  // compile-time coordinate index
+            constexpr int cc = decltype(cc_c)::value;
             const int tt = ch * C + cc;
-            if (tt >= r) break;
+            if (tt >= r) return;
             if (!fresh) {
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
+                auto pass = [&](auto guard) {
 #pragma unroll
-                for (int e = 0; e < NPL; ++e) {
-                    const float4 a4 = Ach[e * NT];
+                    for (int e = 0; e < NPL; ++e) {
+                        const float4 a4 = Ach[e * NT];
 #pragma unroll
-                    for (int q = cc; q < C; ++q) {
-                        const double av = (double)f4_get(a4, q);
-                        if (av != 0.0) {
-                            red[q] = fma(u[e], av, red[q]);
-                            red[C + q] = fma(z[e] * av, av, red[C + q]);
-                        }
+                        for (int q = cc; q < C; ++q)
+                            accum<decltype(guard)::value>(red[q], red[C + q], u[e], z[e], (double)f4_get(a4, q));
                     }
-                }
+                };
+                if (eps > 0.0) pass(std::false_type{});
+                else pass(std::true_type{});
                 block_reduce<NT>(red, sred, buf);
                 fresh = true;
             }
             double x = (double)xs[tt];
-            const double base = a.sum_pos[tt];
+            const double base = ssum[tt];
             double g = (base + alpha * x + a.beta) - red[cc];
             double h = alpha + red[C + cc];
             int inner = 0;
@@ -524,7 +563,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
             }
             if (moved) fresh = false;
             if (tid == 0) xo[tt] = (float)x;
-        }
+        });
     }
     cp_wait<0>();
     __syncthreads();
@@ -541,20 +580,76 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 }
 
 // ---------------------------------------------------------------------------
-// Any-size subproblem, one block each; per-entry t/u/z in global memory (t in
-// t_out, u and z in scratch), each thread owning entries p = tid mod NT.  Same
-// batched scheme: a pass streams every entry once (its 16-byte chunk of the
-// fixed row and its u/z); the final move of the previous coordinate is
-// applied inside the next pass.
-template <int NT>
-__global__ void __launch_bounds__(NT) solve_stream_kernel(const klnmf_solve_args_t a) {
+// Long subproblems (the W side's popular rows): one subproblem per thread-block
+// CLUSTER of k CTAs (k = 1..16).  Each CTA owns a contiguous slice of the
+// entries; per-entry state stays ON CHIP -- NR entries per thread in
+// registers, NS in shared memory -- and only entries beyond the cluster's
+// capacity spill to global memory (t_out / scratch).  Per pass each thread
+// gathers its entries' 16-byte chunks straight from L2/HBM; partial sums are
+// reduced warp -> CTA (shared memory) -> cluster (DSMEM, fixed CTA order), so
+// every CTA sees identical (g, h) and runs the same Newton logic.  A move is
+// applied to the on-chip state immediately.
+namespace cg = cooperative_groups;
+
+constexpr int CL_NT = 512, CL_NR = 8, CL_NS = 12;
+
+struct ClusterRed {
+    double wred[2][CL_NT / 32][NV];
+    double cpart[2][NV];
+    double tot[2][NV];
+};
+
+// Sum of NV values over the cluster; every thread of every CTA gets the same
+// totals (warp transposed reduce, fixed-order CTA sum, fixed-order cluster
+// sum).  Double-buffered: one cluster barrier and two CTA barriers per call.
+__device__ __forceinline__ void cluster_reduce(double (&v)[NV], ClusterRed &R, int &buf, cg::cluster_group &cl,
+                                               int k) {
+    constexpr int NW = CL_NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    TReduce<32>::run(v, lane);
+    if ((lane & 3) == 0) R.wred[buf][w][lane >> 2] = v[0];
+    __syncthreads();
+    if (w == 0 && lane < NV) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) s += R.wred[buf][q][lane];
+        R.cpart[buf][lane] = s;
+    }
+    if (k > 1) {
+        cl.sync();
+        if (w == 0 && lane < NV) {
+            double s = 0.0;
+            for (int c = 0; c < k; ++c) s += cl.map_shared_rank(&R.cpart[buf][0], c)[lane];
+            R.tot[buf][lane] = s;
+        }
+    } else if (w == 0 && lane < NV) {
+        R.tot[buf][lane] = R.cpart[buf][lane];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = R.tot[buf][i];
+    buf ^= 1;
+}
+
+template <int NT, int NR, int NS>
+__global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_args_t a) {
+    static_assert(NT == CL_NT, "reduction buffers are sized for CL_NT");
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.num_blocks();
+    const int cq = (int)cl.block_rank();
+    const int64_t slot = blockIdx.x / k;
+    if (slot >= a.n_items) return;  // uniform over the cluster
+
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float *xs = reinterpret_cast<float *>(smem_raw);  // [2][rps]: input row, result
+    double *Ts = reinterpret_cast<double *>(smem_raw);  // [NS][NT]
+    double *Us = Ts + NS * NT;
+    double *Zs = Us + NS * NT;
+    int2 *VO = reinterpret_cast<int2 *>(Zs + NS * NT);  // (float bits of v, row offset)
+    float *xs = reinterpret_cast<float *>(VO + NS * NT);  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
-    __shared__ double sred[2 * (NT / 32) * NV];
+    __shared__ ClusterRed R;
+
     const int tid = threadIdx.x;
-    const int64_t slot = blockIdx.x;
-    if (slot >= a.n_items) return;
     const int rp = a.rp, r = a.r;
     const float *fixed = static_cast<const float *>(a.fixed);
     float *moving = static_cast<float *>(a.moving);
@@ -562,22 +657,65 @@ __global__ void __launch_bounds__(NT) solve_stream_kernel(const klnmf_solve_args
     const int64_t j = a.items[slot];
     const int64_t lo = a.side.ptr[j];
     const int64_t s = a.side.ptr[j + 1] - lo;
-    double *T = a.t_out + lo;
-    double *U = a.scratch + lo;
-    double *Z = a.scratch + a.side.nnz + lo;
-    const int32_t *vi = a.side.idx + lo;
-    const float *vv = val + lo;
+    const int64_t per = (s + k - 1) / k;
+    const int64_t c0 = min(s, (int64_t)cq * per);
+    const int64_t cn = min(s, c0 + per) - c0;  // entries of this CTA
+    const int64_t base = lo + c0;              // global entry index of local entry 0
     const double eps = a.eps_div, eg = a.eps_grad, alpha = a.alpha;
+    double *Tg = a.t_out + base;  // spilled entries: t in t_out, u/z in scratch
+    double *Ug = a.scratch + base;
+    double *Zg = a.scratch + a.side.nnz + base;
 
-    for (int k = tid; k < r; k += NT) xs[k] = moving[j * rp + a.perm_in[k]];
-    for (int64_t p = tid; p < s; p += NT) {
-        const int64_t q = lo + p;
-        const double tq = a.t_in[a.tmap ? (int64_t)a.tmap[q] : q];
-        T[p] = tq;
-        const double ri = 1.0 / (tq + eps);
-        const double uu = (double)vv[p] * ri;
-        U[p] = uu;
-        Z[p] = uu * ri;
+    __shared__ double ssum[KMAX_RP];
+    for (int kk = tid; kk < r; kk += NT) ssum[kk] = a.sum_pos[kk];
+    for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
+
+    double t[NR], u[NR], z[NR];
+    float v[NR];
+    int off[NR];
+#pragma unroll
+    for (int e = 0; e < NR; ++e) {
+        const int64_t i = tid + (int64_t)e * NT;
+        if (i < cn) {
+            const int64_t g = base + i;
+            off[e] = a.side.idx[g] * rp;
+            v[e] = val[g];
+            const double tq = a.t_in[a.tmap ? (int64_t)a.tmap[g] : g];
+            t[e] = tq;
+            const double ri = fast_rcp(tq + eps);
+            u[e] = (double)v[e] * ri;
+            z[e] = u[e] * ri;
+        } else {
+            off[e] = -1;
+            v[e] = 0.f;
+            t[e] = u[e] = z[e] = 0.0;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < NS; ++e) {
+        const int64_t i = tid + (int64_t)(NR + e) * NT;
+        const int si = e * NT + tid;
+        if (i < cn) {
+            const int64_t g = base + i;
+            const float vv = val[g];
+            VO[si] = make_int2(__float_as_int(vv), a.side.idx[g] * rp);
+            const double tq = a.t_in[a.tmap ? (int64_t)a.tmap[g] : g];
+            const double ri = fast_rcp(tq + eps);
+            Ts[si] = tq;
+            Us[si] = (double)vv * ri;
+            Zs[si] = Us[si] * ri;
+        } else {
+            VO[si] = make_int2(0, -1);
+        }
+    }
+    const int64_t spill0 = (int64_t)(NR + NS) * NT;  // first spilled local entry
+    for (int64_t i = spill0 + tid; i < cn; i += NT) {
+        const int64_t g = base + i;
+        const double tq = a.t_in[a.tmap ? (int64_t)a.tmap[g] : g];
+        const double ri = fast_rcp(tq + eps);
+        Tg[i] = tq;
+        Ug[i] = (double)val[g] * ri;
+        Zg[i] = Ug[i] * ri;
     }
     __syncthreads();
 
@@ -587,105 +725,126 @@ __global__ void __launch_bounds__(NT) solve_stream_kernel(const klnmf_solve_args
     for (int ch = 0; ch < nchunks; ++ch) {
         double red[NV];
         bool fresh = false;
-        double pend_delta = 0.0;  // final move of the previous coordinate, not yet applied
-        int pend_q = 0;
-        for (int cc = 0; cc < C; ++cc) {
+        static_for<0, C>([&](auto cc_c) {  // compile-time coordinate index
+            constexpr int cc = decltype(cc_c)::value;
             const int tt = ch * C + cc;
-            if (tt >= r) break;
+            if (tt >= r) return;
             if (!fresh) {
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                for (int64_t p = tid; p < s; p += NT) {
-                    const float4 A4 = ldg_f4(fixed + (int64_t)vi[p] * rp + ch * C);
-                    double uu = U[p], zz = Z[p];
-                    if (pend_delta != 0.0) {
-                        const double av = (double)f4_get(A4, pend_q);
-                        if (av != 0.0) {
-                            double tn = T[p];
-                            entry_update(pend_delta, av, vv[p], eps, tn, uu, zz);
-                            T[p] = tn;
-                            U[p] = uu;
-                            Z[p] = zz;
-                        }
-                    }
+                auto pass = [&](auto guard) {
+                    auto acc = [&](const float4 &a4, double uu, double zz) {
 #pragma unroll
-                    for (int q = 0; q < C; ++q) {
-                        if (q >= cc) {
-                            const double av = (double)f4_get(A4, q);
-                            if (av != 0.0) {
-                                red[q] = fma(uu, av, red[q]);
-                                red[C + q] = fma(zz * av, av, red[C + q]);
-                            }
-                        }
+                        for (int qq = cc; qq < C; ++qq)
+                            accum<decltype(guard)::value>(red[qq], red[C + qq], uu, zz, (double)f4_get(a4, qq));
+                    };
+#pragma unroll
+                    for (int e = 0; e < NR; ++e)
+                        if (off[e] >= 0) acc(ldg_f4(fixed + off[e] + ch * C), u[e], z[e]);
+#pragma unroll 4
+                    for (int e = 0; e < NS; ++e) {
+                        const int si = e * NT + tid;
+                        const int o = VO[si].y;
+                        if (o >= 0) acc(ldg_f4(fixed + o + ch * C), Us[si], Zs[si]);
                     }
-                }
-                pend_delta = 0.0;
-                block_reduce<NT>(red, sred, buf);
+                    for (int64_t i = spill0 + tid; i < cn; i += NT)
+                        acc(ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i], Zg[i]);
+                };
+                if (eps > 0.0) pass(std::false_type{});
+                else pass(std::true_type{});
+                cluster_reduce(red, R, buf, cl, k);
                 fresh = true;
             }
             double x = (double)xs[tt];
-            const double base = a.sum_pos[tt];
-            double g = (base + alpha * x + a.beta) - red[cc];
+            const double sa = ssum[tt];
+            double g = (sa + alpha * x + a.beta) - red[cc];
             double h = alpha + red[C + cc];
             int inner = 0;
             bool active = enters(g, x, eg);
             bool moved = false;
-            while (active) {
+            while (active) {  // uniform over the cluster
                 bool again = false;
                 const double delta = newton_step(g, h, x, inner, active, again, a, cnt);
-                if (delta != 0.0) moved = true;
-                if (again) {
-                    // apply this step now and re-evaluate the same coordinate
-                    double g2 = 0.0, h2 = 0.0;
-                    for (int64_t p = tid; p < s; p += NT) {
-                        const double av = (double)__ldg(fixed + (int64_t)vi[p] * rp + tt);
-                        double uu = U[p], zz = Z[p];
-                        if (av != 0.0) {
-                            if (delta != 0.0) {
-                                double tn = T[p];
-                                entry_update(delta, av, vv[p], eps, tn, uu, zz);
-                                T[p] = tn;
-                                U[p] = uu;
-                                Z[p] = zz;
+                double ev[NV];
+#pragma unroll
+                for (int i = 0; i < NV; ++i) ev[i] = 0.0;
+                // apply the move (and, if the loop continues, re-evaluate this coordinate)
+                if (delta != 0.0 || again) {
+                    if (delta != 0.0) moved = true;
+#pragma unroll
+                    for (int e = 0; e < NR; ++e) {
+                        if (off[e] >= 0) {
+                            const double av = (double)__ldg(fixed + off[e] + tt);
+                            if (av != 0.0) {
+                                if (delta != 0.0) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
+                                ev[0] = fma(u[e], av, ev[0]);
+                                ev[1] = fma(z[e] * av, av, ev[1]);
                             }
-                            g2 = fma(uu, av, g2);
-                            h2 = fma(zz * av, av, h2);
                         }
                     }
-                    block_reduce2<NT>(g2, h2, sred, buf);
-                    g = (base + alpha * x + a.beta) - g2;
-                    h = alpha + h2;
-                    active = enters(g, x, eg);
-                } else if (delta != 0.0) {
-                    // the loop ends on this step: fuse its update into the next pass
-                    pend_delta = delta;
-                    pend_q = cc;
+#pragma unroll 4
+                    for (int e = 0; e < NS; ++e) {
+                        const int si = e * NT + tid;
+                        const int2 vo = VO[si];
+                        if (vo.y >= 0) {
+                            const double av = (double)__ldg(fixed + vo.y + tt);
+                            if (av != 0.0) {
+                                double tn = Ts[si], uu = Us[si], zz = Zs[si];
+                                if (delta != 0.0) {
+                                    entry_update(delta, av, __int_as_float(vo.x), eps, tn, uu, zz);
+                                    Ts[si] = tn;
+                                    Us[si] = uu;
+                                    Zs[si] = zz;
+                                }
+                                ev[0] = fma(uu, av, ev[0]);
+                                ev[1] = fma(zz * av, av, ev[1]);
+                            }
+                        }
+                    }
+                    for (int64_t i = spill0 + tid; i < cn; i += NT) {
+                        const double av = (double)__ldg(fixed + (int64_t)a.side.idx[base + i] * rp + tt);
+                        if (av != 0.0) {
+                            double tn = Tg[i], uu = Ug[i], zz = Zg[i];
+                            if (delta != 0.0) {
+                                entry_update(delta, av, val[base + i], eps, tn, uu, zz);
+                                Tg[i] = tn;
+                                Ug[i] = uu;
+                                Zg[i] = zz;
+                            }
+                            ev[0] = fma(uu, av, ev[0]);
+                            ev[1] = fma(zz * av, av, ev[1]);
+                        }
+                    }
+                }
+                if (again) {
+                    cluster_reduce(ev, R, buf, cl, k);
+                    g = (sa + alpha * x + a.beta) - ev[0];
+                    h = alpha + ev[1];
+                    active = enters(g, x, eg);  // _kernels.py:78
                 }
             }
             if (moved) fresh = false;
             if (tid == 0) xo[tt] = (float)x;
-        }
-        if (pend_delta != 0.0) {
-            for (int64_t p = tid; p < s; p += NT) {
-                const double av = (double)__ldg(fixed + (int64_t)vi[p] * rp + ch * C + pend_q);
-                if (av != 0.0) {
-                    double tn = T[p], uu = U[p], zz = Z[p];
-                    entry_update(pend_delta, av, vv[p], eps, tn, uu, zz);
-                    T[p] = tn;
-                    U[p] = uu;
-                    Z[p] = zz;
-                }
-            }
-        }
+        });
     }
     __syncthreads();
-    for (int k = tid; k < r; k += NT) moving[j * rp + a.perm_out[k]] = xo[k];
-    if (tid == 0 && a.stats) {
+    if (cq == 0)
+        for (int kk = tid; kk < r; kk += NT) moving[j * rp + a.perm_out[kk]] = xo[kk];
+#pragma unroll
+    for (int e = 0; e < NR; ++e)
+        if (off[e] >= 0) a.t_out[base + tid + (int64_t)e * NT] = t[e];
+#pragma unroll
+    for (int e = 0; e < NS; ++e) {
+        const int si = e * NT + tid;
+        if (VO[si].y >= 0) a.t_out[base + tid + (int64_t)(NR + e) * NT] = Ts[si];
+    }
+    if (cq == 0 && tid == 0 && a.stats) {
         if (cnt.n_inner) atomicAdd(a.stats + KLNMF_STAT_INNER_ITERS, (unsigned long long)cnt.n_inner);
         if (cnt.n_cap) atomicAdd(a.stats + KLNMF_STAT_CAP_HITS, (unsigned long long)cnt.n_cap);
         if (cnt.n_deg) atomicAdd(a.stats + KLNMF_STAT_DEGENERATE, (unsigned long long)cnt.n_deg);
         atomicAdd(a.stats + KLNMF_STAT_PASSES, 1ull);
     }
+    if (k > 1) cl.sync();  // peers may still read this CTA's shared memory
 }
 
 struct FastKernel {
@@ -694,17 +853,23 @@ struct FastKernel {
     void (*fn)(const klnmf_solve_args_t);
     int gpb;           // subproblems per block
     int ring_entries;  // float4 ring slots per thread and stage (NPL)
+    int cluster;       // CTAs per subproblem (cluster kernel), 0 = plain launch
 };
 
-#define WK(L, NPL) {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL>, 128 / (L), NPL}
-#define BK(NT, NPL) {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL>, 1, NPL}
+#define WK(L, NPL) {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL>, 128 / (L), NPL, 0}
+#define BK(NT, NPL) {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL>, 1, NPL, 0}
+#define CK(K, CAP)                                                                                        \
+    {CL_NT * (K), CL_NR + CL_NS, CL_NT, (CAP), solve_cluster_kernel<CL_NT, CL_NR, CL_NS>, 1, 0, (K)}
 const FastKernel kFast[] = {
-    WK(1, 4),  WK(2, 4),   WK(4, 4),   WK(8, 4),   WK(8, 8),   WK(16, 8),
-    WK(32, 8), BK(64, 8),  BK(128, 8), BK(256, 8), BK(512, 8),
-    {1024, 0, 1024, -1, solve_stream_kernel<1024>, 1, 0},
+    WK(1, 4),  WK(2, 4),  WK(4, 4),   WK(8, 4),   WK(8, 8),   WK(16, 8),
+    WK(32, 8), BK(64, 8), BK(128, 8), BK(256, 8), BK(512, 8),
+    CK(1, (int64_t)CL_NT * (CL_NR + CL_NS)),     CK(2, 2ll * CL_NT * (CL_NR + CL_NS)),
+    CK(4, 4ll * CL_NT * (CL_NR + CL_NS)),        CK(8, 8ll * CL_NT * (CL_NR + CL_NS)),
+    CK(16, -1),
 };
 #undef WK
 #undef BK
+#undef CK
 constexpr int kNumFast = sizeof(kFast) / sizeof(kFast[0]);
 
 }  // namespace
@@ -726,12 +891,34 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (kernel_id < 0 || kernel_id >= kNumFast) return set_error_msg(1, "klnmf_solve_fast: bad kernel id");
     if (args->n_items <= 0) return 0;
     if (args->rp % 4 != 0) return set_error_msg(1, "klnmf_solve_fast: rp must be a multiple of 4");
+    if (args->rp > KMAX_RP) return set_error_msg(1, "klnmf_solve_fast: rank above 256 is not supported in fp32 mode");
     const FastKernel &k = kFast[kernel_id];
-    if (k.capacity < 0 && args->scratch == nullptr)
-        return set_error_msg(1, "klnmf_solve_fast: the streaming kernel needs 2*nnz doubles of scratch");
+    const size_t xrow = 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) + 16;
+    if (k.cluster > 0) {
+        if (args->scratch == nullptr)
+            return set_error_msg(1, "klnmf_solve_fast: the cluster kernel needs 2*nnz doubles of scratch");
+        const size_t smem = (size_t)CL_NS * CL_NT * (3 * sizeof(double) + sizeof(int2)) + xrow;
+        KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (k.cluster > 8)
+            KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(args->n_items * k.cluster), 1, 1);
+        cfg.blockDim = dim3((unsigned)k.nt, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = as_stream(stream);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)k.cluster;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        KLNMF_CHECK(cudaLaunchKernelEx(&cfg, k.fn, *args));
+        return 0;
+    }
     const int64_t blocks = (args->n_items + k.gpb - 1) / k.gpb;
     const size_t ring = sizeof(float4) * (size_t)STAGES * (size_t)k.ring_entries * (size_t)k.nt;
-    const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) + 16;
+    const size_t smem = ring + xrow;
     if (smem > 48 * 1024) {
         KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
