@@ -582,16 +582,18 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 // ---------------------------------------------------------------------------
 // Long subproblems (the W side's popular rows): one subproblem per thread-block
 // CLUSTER of k CTAs (k = 1..16).  Each CTA owns a contiguous slice of the
-// entries; per-entry state stays ON CHIP -- NR entries per thread in
-// registers, NS in shared memory -- and only entries beyond the cluster's
-// capacity spill to global memory (t_out / scratch).  Per pass each thread
-// gathers its entries' 16-byte chunks straight from L2/HBM; partial sums are
+// entries and keeps their state ON CHIP -- NR entries per thread in
+// registers, NS in shared memory; only entries beyond the cluster's capacity
+// spill to global memory (t_out / scratch).  At the start of every 4-coordinate
+// chunk each thread cp.async-gathers the chunk of its resident entries into
+// shared memory once; every pass and every move of that chunk then reads it
+// from there (no re-gathers, no scattered scalar loads).  Partial sums are
 // reduced warp -> CTA (shared memory) -> cluster (DSMEM, fixed CTA order), so
-// every CTA sees identical (g, h) and runs the same Newton logic.  A move is
-// applied to the on-chip state immediately.
+// every CTA sees identical (g, h) and runs the same Newton logic.
 namespace cg = cooperative_groups;
 
-constexpr int CL_NT = 512, CL_NR = 8, CL_NS = 12;
+constexpr int CL_NT = 512, CL_NR = 8, CL_NS = 4;
+constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
 
 struct ClusterRed {
     double wred[2][CL_NT / 32][NV];
@@ -633,7 +635,7 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[NV], ClusterRed &R, i
 
 template <int NT, int NR, int NS>
 __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_args_t a) {
-    static_assert(NT == CL_NT, "reduction buffers are sized for CL_NT");
+    static_assert(NT == CL_NT && NR + NS == CL_NE, "buffers are sized for CL_NT / CL_NE");
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.num_blocks();
     const int cq = (int)cl.block_rank();
@@ -641,13 +643,15 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
     if (slot >= a.n_items) return;  // uniform over the cluster
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *Ts = reinterpret_cast<double *>(smem_raw);  // [NS][NT]
+    float4 *cache = reinterpret_cast<float4 *>(smem_raw);    // [NR+NS][NT]: current chunk
+    double *Ts = reinterpret_cast<double *>(cache + (NR + NS) * NT);  // [NS][NT]
     double *Us = Ts + NS * NT;
     double *Zs = Us + NS * NT;
-    int2 *VO = reinterpret_cast<int2 *>(Zs + NS * NT);  // (float bits of v, row offset)
+    int2 *VO = reinterpret_cast<int2 *>(Zs + NS * NT);    // (float bits of v, row offset)
     float *xs = reinterpret_cast<float *>(VO + NS * NT);  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
     __shared__ ClusterRed R;
+    __shared__ double ssum[KMAX_RP];
 
     const int tid = threadIdx.x;
     const int rp = a.rp, r = a.r;
@@ -666,7 +670,6 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
     double *Ug = a.scratch + base;
     double *Zg = a.scratch + a.side.nnz + base;
 
-    __shared__ double ssum[KMAX_RP];
     for (int kk = tid; kk < r; kk += NT) ssum[kk] = a.sum_pos[kk];
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
@@ -706,8 +709,12 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
             Zs[si] = Us[si] * ri;
         } else {
             VO[si] = make_int2(0, -1);
+            Ts[si] = Us[si] = Zs[si] = 0.0;
         }
     }
+    int offs[NS];  // row offsets of the shared-memory entries (for the gathers)
+#pragma unroll
+    for (int e = 0; e < NS; ++e) offs[e] = VO[e * NT + tid].y;
     const int64_t spill0 = (int64_t)(NR + NS) * NT;  // first spilled local entry
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const int64_t g = base + i;
@@ -723,6 +730,16 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
     int buf = 0;
     const int nchunks = (r + C - 1) / C;
     for (int ch = 0; ch < nchunks; ++ch) {
+        // gather this chunk of every resident entry once (own slots only)
+#pragma unroll
+        for (int e = 0; e < NR; ++e)
+            cp_async16(&cache[e * NT + tid], off[e] >= 0 ? fixed + off[e] + ch * C : fixed, off[e] >= 0);
+#pragma unroll
+        for (int e = 0; e < NS; ++e)
+            cp_async16(&cache[(NR + e) * NT + tid], offs[e] >= 0 ? fixed + offs[e] + ch * C : fixed, offs[e] >= 0);
+        cp_commit();
+        cp_wait<0>();
+
         double red[NV];
         bool fresh = false;
         static_for<0, C>([&](auto cc_c) {  // compile-time coordinate index
@@ -739,14 +756,9 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
                             accum<decltype(guard)::value>(red[qq], red[C + qq], uu, zz, (double)f4_get(a4, qq));
                     };
 #pragma unroll
-                    for (int e = 0; e < NR; ++e)
-                        if (off[e] >= 0) acc(ldg_f4(fixed + off[e] + ch * C), u[e], z[e]);
-#pragma unroll 4
-                    for (int e = 0; e < NS; ++e) {
-                        const int si = e * NT + tid;
-                        const int o = VO[si].y;
-                        if (o >= 0) acc(ldg_f4(fixed + o + ch * C), Us[si], Zs[si]);
-                    }
+                    for (int e = 0; e < NR; ++e) acc(cache[e * NT + tid], u[e], z[e]);  // absent: u = z = 0
+#pragma unroll
+                    for (int e = 0; e < NS; ++e) acc(cache[(NR + e) * NT + tid], Us[e * NT + tid], Zs[e * NT + tid]);
                     for (int64_t i = spill0 + tid; i < cn; i += NT)
                         acc(ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i], Zg[i]);
                 };
@@ -773,32 +785,27 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
                     if (delta != 0.0) moved = true;
 #pragma unroll
                     for (int e = 0; e < NR; ++e) {
-                        if (off[e] >= 0) {
-                            const double av = (double)__ldg(fixed + off[e] + tt);
-                            if (av != 0.0) {
-                                if (delta != 0.0) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
-                                ev[0] = fma(u[e], av, ev[0]);
-                                ev[1] = fma(z[e] * av, av, ev[1]);
-                            }
+                        const double av = (double)f4_get(cache[e * NT + tid], cc);
+                        if (off[e] >= 0 && av != 0.0) {
+                            if (delta != 0.0) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
+                            ev[0] = fma(u[e], av, ev[0]);
+                            ev[1] = fma(z[e] * av, av, ev[1]);
                         }
                     }
-#pragma unroll 4
+#pragma unroll
                     for (int e = 0; e < NS; ++e) {
                         const int si = e * NT + tid;
-                        const int2 vo = VO[si];
-                        if (vo.y >= 0) {
-                            const double av = (double)__ldg(fixed + vo.y + tt);
-                            if (av != 0.0) {
-                                double tn = Ts[si], uu = Us[si], zz = Zs[si];
-                                if (delta != 0.0) {
-                                    entry_update(delta, av, __int_as_float(vo.x), eps, tn, uu, zz);
-                                    Ts[si] = tn;
-                                    Us[si] = uu;
-                                    Zs[si] = zz;
-                                }
-                                ev[0] = fma(uu, av, ev[0]);
-                                ev[1] = fma(zz * av, av, ev[1]);
+                        const double av = (double)f4_get(cache[(NR + e) * NT + tid], cc);
+                        if (offs[e] >= 0 && av != 0.0) {
+                            double tn = Ts[si], uu = Us[si], zz = Zs[si];
+                            if (delta != 0.0) {
+                                entry_update(delta, av, __int_as_float(VO[si].x), eps, tn, uu, zz);
+                                Ts[si] = tn;
+                                Us[si] = uu;
+                                Zs[si] = zz;
                             }
+                            ev[0] = fma(uu, av, ev[0]);
+                            ev[1] = fma(zz * av, av, ev[1]);
                         }
                     }
                     for (int64_t i = spill0 + tid; i < cn; i += NT) {
@@ -836,7 +843,7 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
 #pragma unroll
     for (int e = 0; e < NS; ++e) {
         const int si = e * NT + tid;
-        if (VO[si].y >= 0) a.t_out[base + tid + (int64_t)(NR + e) * NT] = Ts[si];
+        if (offs[e] >= 0) a.t_out[base + tid + (int64_t)(NR + e) * NT] = Ts[si];
     }
     if (cq == 0 && tid == 0 && a.stats) {
         if (cnt.n_inner) atomicAdd(a.stats + KLNMF_STAT_INNER_ITERS, (unsigned long long)cnt.n_inner);
@@ -897,7 +904,8 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (k.cluster > 0) {
         if (args->scratch == nullptr)
             return set_error_msg(1, "klnmf_solve_fast: the cluster kernel needs 2*nnz doubles of scratch");
-        const size_t smem = (size_t)CL_NS * CL_NT * (3 * sizeof(double) + sizeof(int2)) + xrow;
+        const size_t smem = (size_t)CL_NE * CL_NT * sizeof(float4) +
+                            (size_t)CL_NS * CL_NT * (3 * sizeof(double) + sizeof(int2)) + xrow;
         KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (k.cluster > 8)
             KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
