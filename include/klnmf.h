@@ -127,6 +127,17 @@ int klnmf_fast_kernel_count(void);
 /* capacity (max nnz per subproblem) and lanes of kernel_id; capacity < 0 = unbounded */
 int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t *lanes, int32_t *npl);
 
+/* Long-row bucket (capacity -1 in klnmf_fast_kernel_info): a persistent
+ * cooperative kernel, one CTA per SM, each row spread over G CTAs so its
+ * per-entry state stays on chip; reductions of a row group go through `sync`
+ * (global memory).  klnmf_coop_info reports the CTA count, entries per CTA and
+ * sync bytes per row group for padded rank rp; the caller packs the bucket's
+ * rows into waves: schedule is int32[n_waves][n_ctas][4] = (index into
+ * args->items or -1, rank in group, group size G, group id). */
+int klnmf_coop_info(int32_t rp, int64_t *entries_per_cta, int32_t *n_ctas, int64_t *sync_bytes_per_group);
+int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *schedule, int32_t n_waves, int32_t n_ctas,
+                     void *sync, int64_t n_groups, void *stream);
+
 /* row sums of a device factor by position (n_items, rp): exact = numpy pairwise over
  * fp64 items in order; fast = deterministic fp64 two-level sum of fp32 items. */
 int klnmf_row_sums_exact(const double *fac, int64_t n_items, int32_t rp, int32_t r,

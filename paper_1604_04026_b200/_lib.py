@@ -31,6 +31,8 @@ EXPORTS = (
     "klnmf_solve_fast",
     "klnmf_fast_kernel_count",
     "klnmf_fast_kernel_info",
+    "klnmf_coop_info",
+    "klnmf_solve_coop",
     "klnmf_row_sums_exact",
     "klnmf_row_sums_fast",
     "klnmf_layout_to_device",
@@ -99,6 +101,8 @@ _SIGS = {
     "klnmf_solve_fast": ([ctypes.POINTER(SolveArgs), INT, P], INT),
     "klnmf_fast_kernel_count": ([], INT),
     "klnmf_fast_kernel_info": ([INT, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)], INT),
+    "klnmf_coop_info": ([I32, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I64)], INT),
+    "klnmf_solve_coop": ([ctypes.POINTER(SolveArgs), P, I32, I32, P, I64, P], INT),
     "klnmf_row_sums_exact": ([P, I64, I32, I32, P, P], INT),
     "klnmf_row_sums_fast": ([P, I64, I32, I32, P, P], INT),
     "klnmf_layout_to_device": ([P, I64, I64, P, I32, P, INT, P], INT),
@@ -143,6 +147,14 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def coop_info(rp: int):
+    """(entries per CTA, CTAs of the cooperative long-row kernel, sync bytes per row group)."""
+    lib = load()
+    e, n, b = I64(), I32(), I64()
+    check(lib.klnmf_coop_info(int(rp), ctypes.byref(e), ctypes.byref(n), ctypes.byref(b)), "klnmf_coop_info")
+    return e.value, n.value, b.value
 
 
 def fast_kernels():

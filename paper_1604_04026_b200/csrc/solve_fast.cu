@@ -633,16 +633,12 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[NV], ClusterRed &R, i
     buf ^= 1;
 }
 
-template <int NT, int NR, int NS>
-__global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_args_t a) {
+// One subproblem's slice on one CTA: rank cq of the k CTAs sharing it.
+// `reduce(v)` sums NV values over the k CTAs (identical result in all).
+template <int NT, int NR, int NS, typename ReduceFn>
+__device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t slot, int cq, int k,
+                                            ReduceFn &&reduce, unsigned char *smem_raw, const double *ssum) {
     static_assert(NT == CL_NT && NR + NS == CL_NE, "buffers are sized for CL_NT / CL_NE");
-    cg::cluster_group cl = cg::this_cluster();
-    const int k = (int)cl.num_blocks();
-    const int cq = (int)cl.block_rank();
-    const int64_t slot = blockIdx.x / k;
-    if (slot >= a.n_items) return;  // uniform over the cluster
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *cache = reinterpret_cast<float4 *>(smem_raw);    // [NR+NS][NT]: current chunk
     double *Ts = reinterpret_cast<double *>(cache + (NR + NS) * NT);  // [NS][NT]
     double *Us = Ts + NS * NT;
@@ -650,8 +646,6 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
     int2 *VO = reinterpret_cast<int2 *>(Zs + NS * NT);    // (float bits of v, row offset)
     float *xs = reinterpret_cast<float *>(VO + NS * NT);  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
-    __shared__ ClusterRed R;
-    __shared__ double ssum[KMAX_RP];
 
     const int tid = threadIdx.x;
     const int rp = a.rp, r = a.r;
@@ -670,7 +664,6 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
     double *Ug = a.scratch + base;
     double *Zg = a.scratch + a.side.nnz + base;
 
-    for (int kk = tid; kk < r; kk += NT) ssum[kk] = a.sum_pos[kk];
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
     double t[NR], u[NR], z[NR];
@@ -727,7 +720,6 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
     __syncthreads();
 
     Counters cnt;
-    int buf = 0;
     const int nchunks = (r + C - 1) / C;
     for (int ch = 0; ch < nchunks; ++ch) {
         // gather this chunk of every resident entry once (own slots only)
@@ -764,7 +756,7 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
                 };
                 if (eps > 0.0) pass(std::false_type{});
                 else pass(std::true_type{});
-                cluster_reduce(red, R, buf, cl, k);
+                reduce(red);
                 fresh = true;
             }
             double x = (double)xs[tt];
@@ -824,7 +816,7 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
                     }
                 }
                 if (again) {
-                    cluster_reduce(ev, R, buf, cl, k);
+                    reduce(ev);
                     g = (sa + alpha * x + a.beta) - ev[0];
                     h = alpha + ev[1];
                     active = enters(g, x, eg);  // _kernels.py:78
@@ -851,7 +843,111 @@ __global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_
         if (cnt.n_deg) atomicAdd(a.stats + KLNMF_STAT_DEGENERATE, (unsigned long long)cnt.n_deg);
         atomicAdd(a.stats + KLNMF_STAT_PASSES, 1ull);
     }
+}
+
+template <int NT, int NR, int NS>
+__global__ void __launch_bounds__(NT, 1) solve_cluster_kernel(const klnmf_solve_args_t a) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.num_blocks();
+    const int cq = (int)cl.block_rank();
+    const int64_t slot = blockIdx.x / k;
+    if (slot >= a.n_items) return;  // uniform over the cluster
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ ClusterRed R;
+    __shared__ double ssum[KMAX_RP];
+    for (int kk = threadIdx.x; kk < a.r; kk += NT) ssum[kk] = a.sum_pos[kk];
+    int buf = 0;
+    solve_slice<NT, NR, NS>(
+        a, slot, cq, k, [&](double (&v)[NV]) { cluster_reduce(v, R, buf, cl, k); }, smem_raw, ssum);
     if (k > 1) cl.sync();  // peers may still read this CTA's shared memory
+}
+
+// ---------------------------------------------------------------------------
+// Rows too long for one 16-CTA cluster: a persistent COOPERATIVE kernel (all
+// CTAs co-resident, one per SM).  A host-built schedule packs the rows into
+// waves; a row spans as many CTAs as its entries need, so all per-entry state
+// stays on chip.  The per-pass reduction of a row group goes through global
+// memory: each CTA publishes its partial sums, bumps the group's monotonic
+// counter and waits until all G members of the round have arrived.  Waits
+// only point to rows of the same or an earlier wave, all CTAs are resident,
+// so the schedule cannot deadlock.
+struct CoopGroup {
+    double *slots;       // [2][G][NV] partials, double-buffered by round parity
+    unsigned *counter;   // arrivals, G per round
+    int G, rank;
+    unsigned round;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void coop_reduce(double (&v)[NV], ClusterRed &R, int &buf, CoopGroup &g) {
+    constexpr int NW = CL_NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    TReduce<32>::run(v, lane);
+    if ((lane & 3) == 0) R.wred[buf][w][lane >> 2] = v[0];
+    __syncthreads();
+    if (w == 0) {
+        double part = 0.0;
+        if (lane < NV) {
+#pragma unroll
+            for (int q = 0; q < NW; ++q) part += R.wred[buf][q][lane];
+        }
+        if (g.G > 1) {
+            double *cur = g.slots + (size_t)(g.round & 1) * g.G * NV;
+            if (lane < NV) {
+                __stcg(cur + (size_t)g.rank * NV + lane, part);
+                __threadfence();
+            }
+            __syncwarp();
+            const unsigned target = (unsigned)g.G * (g.round + 1);
+            if (lane == 0) {
+                atomicAdd(g.counter, 1u);
+                while (ld_acquire(g.counter) < target) __nanosleep(64);
+            }
+            __syncwarp();
+            if (lane < NV) {
+                (void)ld_acquire(g.counter);
+                double s = 0.0;
+                for (int c = 0; c < g.G; ++c) s += __ldcg(cur + (size_t)c * NV + lane);
+                R.tot[buf][lane] = s;
+            }
+        } else if (lane < NV) {
+            R.tot[buf][lane] = part;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = R.tot[buf][i];
+    buf ^= 1;
+    ++g.round;
+}
+
+// schedule: [n_waves][gridDim.x] int4 (item slot or -1, rank, G, group id);
+// sync: per group, a 128-byte counter line then 2*CL_MAXG*NV doubles.
+constexpr int CL_MAXG = 256;
+constexpr size_t COOP_GROUP_BYTES = 128 + 2 * CL_MAXG * NV * sizeof(double);
+
+template <int NT, int NR, int NS>
+__global__ void __launch_bounds__(NT, 1) solve_coop_kernel(const klnmf_solve_args_t a, const int4 *schedule,
+                                                           int n_waves, unsigned char *sync) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ ClusterRed R;
+    __shared__ double ssum[KMAX_RP];
+    for (int kk = threadIdx.x; kk < a.r; kk += NT) ssum[kk] = a.sum_pos[kk];
+    int buf = 0;
+    for (int wv = 0; wv < n_waves; ++wv) {
+        const int4 job = schedule[(size_t)wv * gridDim.x + blockIdx.x];
+        if (job.x < 0) continue;
+        unsigned char *gb = sync + (size_t)job.w * COOP_GROUP_BYTES;
+        CoopGroup g{reinterpret_cast<double *>(gb + 128), reinterpret_cast<unsigned *>(gb), job.z, job.y, 0u};
+        __syncthreads();  // shared buffers of the previous row are no longer read
+        solve_slice<NT, NR, NS>(
+            a, job.x, job.y, job.z, [&](double (&v)[NV]) { coop_reduce(v, R, buf, g); }, smem_raw, ssum);
+    }
 }
 
 struct FastKernel {
@@ -872,7 +968,9 @@ const FastKernel kFast[] = {
     WK(32, 8), BK(64, 8), BK(128, 8), BK(256, 8), BK(512, 8),
     CK(1, (int64_t)CL_NT * (CL_NR + CL_NS)),     CK(2, 2ll * CL_NT * (CL_NR + CL_NS)),
     CK(4, 4ll * CL_NT * (CL_NR + CL_NS)),        CK(8, 8ll * CL_NT * (CL_NR + CL_NS)),
-    CK(16, -1),
+    CK(16, 16ll * CL_NT * (CL_NR + CL_NS)),
+    // unbounded: the cooperative long-row kernel (klnmf_solve_coop, schedule built by the caller)
+    {CL_NT, CL_NR + CL_NS, CL_NT, -1, nullptr, 1, 0, -1},
 };
 #undef WK
 #undef BK
@@ -900,6 +998,7 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (args->rp % 4 != 0) return set_error_msg(1, "klnmf_solve_fast: rp must be a multiple of 4");
     if (args->rp > KMAX_RP) return set_error_msg(1, "klnmf_solve_fast: rank above 256 is not supported in fp32 mode");
     const FastKernel &k = kFast[kernel_id];
+    if (k.cluster < 0) return set_error_msg(1, "klnmf_solve_fast: the long-row bucket runs through klnmf_solve_coop");
     const size_t xrow = 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) + 16;
     if (k.cluster > 0) {
         if (args->scratch == nullptr)
@@ -932,5 +1031,47 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     }
     k.fn<<<(unsigned)blocks, k.nt, smem, as_stream(stream)>>>(*args);
     KLNMF_CHECK_LAUNCH("klnmf_solve_fast");
+    return 0;
+}
+
+namespace klnmf {
+namespace {
+inline size_t coop_smem(int rp) {
+    return (size_t)CL_NE * CL_NT * sizeof(float4) + (size_t)CL_NS * CL_NT * (3 * sizeof(double) + sizeof(int2)) +
+           2 * sizeof(float) * (size_t)(rp | 1) + 16;
+}
+}  // namespace
+}  // namespace klnmf
+
+extern "C" int klnmf_coop_info(int32_t rp, int64_t *entries_per_cta, int32_t *n_ctas, int64_t *sync_bytes_per_group) {
+    auto fn = solve_coop_kernel<CL_NT, CL_NR, CL_NS>;
+    const size_t smem = coop_smem(rp);
+    KLNMF_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 0, per_sm = 0;
+    KLNMF_CHECK(cudaGetDevice(&dev));
+    KLNMF_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    KLNMF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CL_NT, smem));
+    *entries_per_cta = (int64_t)CL_NT * CL_NE;
+    *n_ctas = sms * per_sm < CL_MAXG ? sms * per_sm : CL_MAXG;
+    *sync_bytes_per_group = (int64_t)COOP_GROUP_BYTES;
+    return 0;
+}
+
+extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *schedule, int32_t n_waves,
+                                int32_t n_ctas, void *sync, int64_t n_groups, void *stream) {
+    if (n_waves <= 0 || args->n_items <= 0) return 0;
+    if (args->rp > KMAX_RP) return set_error_msg(1, "klnmf_solve_coop: rank above 256 is not supported");
+    if (args->scratch == nullptr) return set_error_msg(1, "klnmf_solve_coop: needs 2*nnz doubles of scratch");
+    cudaStream_t st = as_stream(stream);
+    auto fn = solve_coop_kernel<CL_NT, CL_NR, CL_NS>;
+    const size_t smem = coop_smem(args->rp);
+    KLNMF_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    KLNMF_CHECK(cudaMemsetAsync(sync, 0, (size_t)n_groups * COOP_GROUP_BYTES, st));
+    klnmf_solve_args_t a = *args;
+    const int4 *sched = static_cast<const int4 *>(schedule);
+    unsigned char *sy = static_cast<unsigned char *>(sync);
+    int nw = n_waves;
+    void *kargs[] = {&a, &sched, &nw, &sy};
+    KLNMF_CHECK(cudaLaunchCooperativeKernel((const void *)fn, dim3((unsigned)n_ctas), dim3(CL_NT), kargs, smem, st));
     return 0;
 }

@@ -79,6 +79,7 @@ class SidePlan:
     items: torch.Tensor       # int32, this rank's items, sorted by nnz descending
     buckets: list             # [(kernel_id, start, count)], largest first
     tmap: torch.Tensor | None = None  # int32[nnz] entry -> position in the other side
+    coop: tuple | None = None  # long-row bucket: (schedule, n_waves, n_ctas, sync, n_groups)
 
     def side_struct(self) -> _lib.Side:
         return _lib.Side(self.ptr.data_ptr(), self.idx.data_ptr(), self.val.data_ptr(),
@@ -139,6 +140,9 @@ class DevicePlan:
                 "W": self._make_side("W", csr_ptr, csr_idx, csr_val, self.m, self.n, csr_ptr_host,
                                      map_csr2csc if self.fp32 else None),
             }
+            if self.fp32:
+                for sp in self.sides.values():
+                    self._build_coop(sp)
             self._track("V_csc", csc_ptr, csc_idx, csc_val)
             self._track("V_csr", csr_ptr, csr_idx, csr_val)
             if self.fp32:
@@ -155,6 +159,8 @@ class DevicePlan:
                 self.t = {"csc": torch.zeros(nz, dtype=torch.float64, device=dev),
                           "csr": torch.zeros(nz, dtype=torch.float64, device=dev)}
                 self._track("t", self.t["csc"], self.t["csr"])
+                # scratch backs per-entry state that cannot stay on chip (rows
+                # longer than the whole GPU's on-chip capacity, long-row bucket)
                 need_stream = any(b[0] == self._stream_kernel_id() and b[2] > 0
                                   for s in self.sides.values() for b in s.buckets)
                 self.scratch = torch.empty(2 * nz if need_stream else 1, dtype=torch.float64, device=dev)
@@ -203,6 +209,39 @@ class DevicePlan:
         assert start == hi - lo, (start, hi, lo)
         return SidePlan(name, ptr, idx, val, int(n_fix), int(n_mov), int(ptr[-1].item()) if n_mov else 0,
                         np.asarray(ptr_host, dtype=np.int64), ranges, items, buckets, tmap)
+
+    def _build_coop(self, sp: SidePlan) -> None:
+        """Pack the long-row bucket into waves of the cooperative kernel.
+
+        Each row gets G = ceil(nnz / entries_per_cta) CTAs (capped at the CTA
+        count: beyond that its state spills to global memory); rows are taken
+        largest first and placed first-fit into waves of n_ctas CTAs."""
+        kid = self._stream_kernel_id()
+        start, count = next(((st, c) for k, st, c in sp.buckets if k == kid), (0, 0))
+        if count == 0:
+            return
+        per_cta, n_ctas, group_bytes = _lib.coop_info(self.rp)
+        rows = sp.items[start:start + count].cpu().numpy()
+        sizes = np.diff(sp.ptr_host)[rows]
+        waves = []  # [free CTAs, list of (slot, c0, G)]
+        for q, sz in enumerate(sizes):
+            G = int(min(n_ctas, max(1, -(-int(sz) // per_cta))))
+            for w in waves:
+                if w[0] >= G:
+                    break
+            else:
+                w = [n_ctas, []]
+                waves.append(w)
+            w[1].append((q, n_ctas - w[0], G))
+            w[0] -= G
+        sched = np.full((len(waves), n_ctas, 4), -1, dtype=np.int32)
+        for wi, (_, jobs) in enumerate(waves):
+            for q, c0, G in jobs:
+                for rank in range(G):
+                    sched[wi, c0 + rank] = (q, rank, G, q)
+        sched_d = torch.from_numpy(sched).to(self.dev)
+        sync = torch.empty(count * group_bytes, dtype=torch.uint8, device=self.dev)
+        sp.coop = (sched_d, len(waves), n_ctas, sync, count)
 
     def _h2d_i32(self, dst: torch.Tensor, arr) -> None:
         host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32))
@@ -335,8 +374,14 @@ class DevicePlan:
                 a.items = item_base + 4 * start
                 a.n_items = count
                 ev = self._event_pair(events)
-                _lib.check(_lib.load().klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr),
-                           "klnmf_solve_fast")
+                if kid == self._stream_kernel_id():
+                    sched, n_waves, n_ctas, sync, n_groups = side.coop
+                    _lib.check(_lib.load().klnmf_solve_coop(ctypes.byref(a), sched.data_ptr(), n_waves, n_ctas,
+                                                            sync.data_ptr(), n_groups, self.stream_ptr),
+                               "klnmf_solve_coop")
+                else:
+                    _lib.check(_lib.load().klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr),
+                               "klnmf_solve_fast")
                 if ev is not None:
                     ev[1].record(torch.cuda.current_stream(self.dev))
                     events.append((which, kid, ev[0], ev[1]))

@@ -201,7 +201,8 @@ def test_every_bucket_kernel(cuda_ok):
     sizes = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257,
              511, 512, 513, 1023, 1024, 1025, 2047, 2048, 2049, 3000, 4095, 4097, 5999, 10240, 10241, 20000,
              40000, 60000]
-    sizes = sizes * 3 + [100000, 180000]  # the 16-CTA cluster kernel, the last one spilling to global
+    # 16-CTA cluster; cooperative long-row kernel (several rows per wave, multi-CTA groups)
+    sizes = sizes * 3 + [90000, 100000, 180000, 199000]
     rows, cols = [], []
     for j, s in enumerate(sizes):
         rr = np.sort(rng.choice(n, size=s, replace=False))
