@@ -46,7 +46,7 @@ def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -337,6 +337,7 @@ def run_ours(args):
     peak, peak_kind = peaks()
     if not kernel_ms:
         kernel_ms[("F", -2)] = [0.0]
+    kinfo_default = (-2, 0, 0, 0)
     dom = max(kernel_ms.items(), key=lambda kv: np.sum(kv[1]))
     (dside, dkid), dms = dom
     sp = plan.sides[dside]
@@ -357,8 +358,8 @@ def run_ours(args):
     it_bytes = iteration_bytes(spec.n, spec.m, V.nnz, r)
     kernel_table = {
         f"{s}:{k}": {"ms_per_step": float(np.sum(v)) / args.steps,
-                     "lanes": next(x for x in plan.fast_kernels if x[0] == k)[2]}
-        for (s, k), v in sorted(kernel_ms.items(), key=lambda kv: -np.sum(kv[1]))
+                     "lanes": next((x for x in plan.fast_kernels if x[0] == k), kinfo_default)[2]}
+        for (s, k), v in sorted(kernel_ms.items(), key=lambda kv: -np.sum(kv[1])) if k >= -1
     }
 
     line = None

@@ -112,22 +112,23 @@ __device__ __forceinline__ double newton_step(double g, double h, double &x, int
     return delta;
 }
 
-// 1/x: MUFU approximation refined by two Newton steps (<= 1 ulp); x == 0
-// (only possible with eps_div == 0) returns inf like the IEEE division.
+// 1/x: MUFU approximation refined by one Newton step (relative error ~1e-14,
+// far below the fp32 storage rounding of this mode); x == 0 (only possible
+// with eps_div == 0) returns inf like the IEEE division.
 __device__ __forceinline__ double fast_rcp(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
+    const double e = fma(-x, r, 1.0);
     r = fma(r, e, r);
     return x == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : r;
 }
 
+// Move of the visited coordinate by delta at an entry with a != 0: the
+// maintained product and its derived u = v/(t+eps), z = u/(t+eps).  The clamp
+// at 0 is the reference's (_kernels.py:105-106).
 __device__ __forceinline__ void entry_update(double delta, double av, float v, double eps, double &t, double &u,
                                              double &z) {
-    double tn = fma(delta, av, t);
-    if (tn < 0.0) tn = 0.0;
+    const double tn = fmax(fma(delta, av, t), 0.0);
     t = tn;
     const double ri = fast_rcp(tn + eps);
     u = (double)v * ri;
