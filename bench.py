@@ -303,7 +303,6 @@ def run_ours(args):
 
     plan.take_stats()
     step_ms = []
-    per_step_events = []
     with ClockSampler(-1 if args.no_clocks else local) as clocks:
         for _ in range(args.steps):
             if not args.no_flush:
@@ -314,13 +313,13 @@ def run_ours(args):
             e0.record(stream)
             step(ev)
             e1.record(stream)
-            per_step_events.append((e0, e1, ev))
-        torch.cuda.synchronize(dev)
-    for e0, e1, ev in per_step_events:
-        step_ms.append(e0.elapsed_time(e1))
-        for (side, kid, a, b) in ev or []:
-            kernel_ms.setdefault((side, kid), []).append(a.elapsed_time(b))
-            launch_count[0] += 1
+            # per-kernel events are CUDA-graph nodes re-recorded by each replay:
+            # read them before the next step (device time is unaffected)
+            torch.cuda.synchronize(dev)
+            step_ms.append(e0.elapsed_time(e1))
+            for (side, kid, a, b) in ev or []:
+                kernel_ms.setdefault((side, kid), []).append(a.elapsed_time(b))
+                launch_count[0] += 1
     launch_count[0] += plan.aux_launches_per_step * args.steps
     st = plan.take_stats()
     total_ms = float(np.sum(step_ms))

@@ -53,6 +53,10 @@ extern "C" {
 
 int klnmf_abi_version(void);
 const char *klnmf_last_error(void);
+/* Record a CUDA event on a stream; external != 0 makes a recording inside a
+ * CUDA-graph capture a real (timing-capable) event node, re-recorded by every
+ * replay (used for per-kernel timing of captured half-steps). */
+int klnmf_event_record(void *event, void *stream, int external);
 
 /* ------------------------------------------------------------------ */
 /* 1. Drop-in host entry points (reference layout, fp64, bit-exact).   */

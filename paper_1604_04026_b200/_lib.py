@@ -24,6 +24,7 @@ INT = ctypes.c_int
 EXPORTS = (
     "klnmf_abi_version",
     "klnmf_last_error",
+    "klnmf_event_record",
     "klnmf_sweep_range",
     "klnmf_kl_data_term",
     "klnmf_row_sums",
@@ -94,6 +95,7 @@ class SolveArgs(ctypes.Structure):
 _SIGS = {
     "klnmf_abi_version": ([], INT),
     "klnmf_last_error": ([], ctypes.c_char_p),
+    "klnmf_event_record": ([P, P, INT], INT),
     "klnmf_sweep_range": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, P], INT),
     "klnmf_kl_data_term": ([P, P, P, P, P, D, I64, I64, I64, P], INT),
     "klnmf_row_sums": ([P, I64, I64, P], INT),

@@ -27,6 +27,28 @@ int set_error_msg(int code, const char *msg) {
     return code;
 }
 
+cudaError_t ensure_smem(const void *fn, size_t bytes) {
+    struct Entry {
+        const void *fn;
+        size_t bytes;
+    };
+    static Entry cache[64];
+    static int n = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void *key = static_cast<const char *>(fn) + dev;  // attributes are per device
+    for (int i = 0; i < n; ++i)
+        if (cache[i].fn == key) {
+            if (cache[i].bytes >= bytes) return cudaSuccess;
+            const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+            if (e == cudaSuccess) cache[i].bytes = bytes;
+            return e;
+        }
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess && n < 64) cache[n++] = Entry{key, bytes};
+    return e;
+}
+
 int row_sums_ref_layout(const double *fac_dev, int64_t r, int64_t n, double *out_dev, cudaStream_t st);
 
 namespace {
@@ -76,6 +98,15 @@ using namespace klnmf;
 extern "C" int klnmf_abi_version(void) { return KLNMF_ABI_VERSION; }
 
 extern "C" const char *klnmf_last_error(void) { return g_err; }
+
+extern "C" int klnmf_event_record(void *event, void *stream, int external) {
+    cudaEvent_t ev = static_cast<cudaEvent_t>(event);
+    if (external)
+        KLNMF_CHECK(cudaEventRecordWithFlags(ev, as_stream(stream), cudaEventRecordExternal));
+    else
+        KLNMF_CHECK(cudaEventRecord(ev, as_stream(stream)));
+    return 0;
+}
 
 extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
                                  const double *at, const double *sum_a, double *moving, int64_t j_lo, int64_t j_hi,

@@ -26,6 +26,10 @@ int set_error_msg(int code, const char *msg);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size,
+// so launch paths replayed under CUDA-graph capture issue no attribute calls.
+cudaError_t ensure_smem(const void *fn, size_t bytes);
+
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
 __device__ __forceinline__ float4 ldg_f4(const float *p) {

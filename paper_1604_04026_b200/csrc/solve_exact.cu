@@ -285,10 +285,7 @@ extern "C" int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream) {
     if (args->n_items <= 0) return 0;
     const int64_t blocks = (args->n_items + EXACT_WPB - 1) / EXACT_WPB;
     const size_t smem = sizeof(double) * (size_t)EXACT_WPB * (size_t)args->rp;
-    if (smem > 48 * 1024) {
-        KLNMF_CHECK(cudaFuncSetAttribute(solve_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-    }
+    if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)solve_exact_kernel, smem));
     solve_exact_kernel<<<(unsigned)blocks, EXACT_WPB * 32, smem, as_stream(stream)>>>(*args);
     KLNMF_CHECK_LAUNCH("solve_exact_kernel");
     return 0;

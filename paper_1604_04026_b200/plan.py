@@ -172,6 +172,12 @@ class DevicePlan:
             self.stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
             self.sum_pos = torch.zeros(self.rp, dtype=torch.float64, device=dev)
             self._perm = torch.zeros(3, self.rp, dtype=torch.int32, device=dev)
+            self._perm_host = torch.zeros(3, self.rp, dtype=torch.int32).pin_memory()
+            self._perm_event = None
+            self.use_graphs = True
+            self._capturing = False
+            self._graphs = {}
+            self._warm = set()
             self._pos = torch.zeros(2, self.rp, dtype=torch.int32, device=dev)
 
     # ------------------------------------------------------------------
@@ -324,12 +330,17 @@ class DevicePlan:
         (W, the next iteration's order; defaults to `ids`).  `sums_pos`
         overrides the device row sums (the public sweep() passes the
         caller's sums, solver.py:165).  With `events` (a list), a CUDA event
-        pair is recorded around every solver launch and appended as
-        (which, kernel_id, start, end).
+        pair around every solver launch is appended as (which, kernel_id,
+        start, end); with CUDA graphs the pairs are graph nodes, re-recorded
+        by every replay.
+
+        Every pointer of a half-step is fixed for the plan's lifetime; only
+        the contents of the visit-order maps (and the row sums) change.  The
+        launch sequence of each side is therefore captured once into a CUDA
+        graph and replayed, the maps arriving by an asynchronous pinned copy.
         """
         ids = np.asarray(ids, dtype=np.int64)
         fixed_name = "W" if which == "F" else "F"
-        side = self.sides[which]
         if self.order[fixed_name] is None or not np.array_equal(self.order[fixed_name], ids):
             raise RuntimeError(f"fixed factor {fixed_name} is not stored in the visit order")
         o_mov = self.order[which]
@@ -337,15 +348,81 @@ class DevicePlan:
         perm_in = np.argsort(o_mov)[ids]
         perm_out = np.argsort(out_order)[ids]
         nat_pos = np.argsort(ids)
-        host = np.stack([self._padded(perm_in), self._padded(perm_out), self._padded(nat_pos)])
-        self._perm.copy_(torch.from_numpy(host))
-        if sums_pos is None:
-            self.row_sums_pos(fixed_name)
-        else:
+        self._stage_perms(np.stack([self._padded(perm_in), self._padded(perm_out), self._padded(nat_pos)]))
+        dev_sums = sums_pos is None
+        if not dev_sums:
             sp = np.zeros(self.rp)
             sp[: self.r] = np.asarray(sums_pos, dtype=np.float64)
             self.sum_pos.copy_(torch.from_numpy(sp))
+        if self.fp32:
+            need = "csr" if which == "F" else "csc"
+            if self.t_current != need:
+                self._init_t(need)
+        key = (which, float(alpha), float(beta), tol, dev_sums, events is not None)
+        if self.use_graphs:
+            entry = self._graphs.get(key)
+            if entry is None:
+                entry = self._capture(key)
+            if entry is not None:
+                graph, evs = entry
+                graph.replay()
+                if events is not None:
+                    events.extend(evs)
+            else:
+                self._launch(which, alpha, beta, tol, dev_sums, events)
+        else:
+            self._launch(which, alpha, beta, tol, dev_sums, events)
+        if self.fp32:
+            self.t_current = "csc" if which == "F" else "csr"
+        self.order[which] = np.asarray(out_order, dtype=np.int64).copy()
+        if self.world > 1:
+            self._exchange(which)
 
+    def _stage_perms(self, host: np.ndarray) -> None:
+        """Visit-order maps -> device through a pinned buffer (no host stall).
+
+        The pinned buffer is reused only after the previous copy completed
+        (tracked by an event), so a running copy never sees new contents."""
+        if self._perm_event is not None:
+            self._perm_event.synchronize()
+        self._perm_host.numpy()[...] = host
+        self._perm.copy_(self._perm_host, non_blocking=True)
+        if self._perm_event is None:
+            self._perm_event = torch.cuda.Event()
+        self._perm_event.record(torch.cuda.current_stream(self.dev))
+
+    def _capture(self, key):
+        """Capture one side's launch sequence (after one eager warm-up run of
+        it, so the library's one-time function attributes are already set)."""
+        which, alpha, beta, tol, dev_sums, with_events = key
+        if key not in self._warm:
+            self._warm.add(key)
+            return None  # run eagerly this time
+        graph = torch.cuda.CUDAGraph()
+        capture_stream = torch.cuda.Stream(self.dev)
+        evs: list = []
+        saved = self.stream_ptr
+        try:
+            with torch.cuda.graph(graph, stream=capture_stream):
+                self.stream_ptr = capture_stream.cuda_stream
+                self._capturing = True
+                self._launch(which, alpha, beta, tol, dev_sums, evs if with_events else None)
+        except Exception:  # capture unsupported here: stay eager
+            self.use_graphs = False
+            return None
+        finally:
+            self.stream_ptr = saved
+            self._capturing = False
+        self._graphs[key] = (graph, evs)
+        return self._graphs[key]
+
+    def _launch(self, which, alpha, beta, tol, dev_sums, events) -> None:
+        """Enqueue one half-step on self.stream_ptr: fixed-factor row sums,
+        then one solver launch per non-empty nnz bucket (largest first)."""
+        fixed_name = "W" if which == "F" else "F"
+        side = self.sides[which]
+        if dev_sums:
+            self.row_sums_pos(fixed_name)
         a = _lib.SolveArgs()
         a.side = side.side_struct()
         a.fixed = self.factors[fixed_name].data_ptr()
@@ -360,55 +437,47 @@ class DevicePlan:
         a.inner_cap = int(tol.inner_iter_cap)
         a.stats = self.stats.data_ptr()
         a.scratch = self.scratch.data_ptr()
-        item_base = side.items.data_ptr()
         if self.fp32:
             need = "csr" if which == "F" else "csc"
-            if self.t_current != need:
-                self._init_t(need)
             a.tmap = side.tmap.data_ptr()
             a.t_in = self.t[need].data_ptr()
             a.t_out = self.t["csc" if which == "F" else "csr"].data_ptr()
-            for kid, start, count in side.buckets:
-                if count == 0:
-                    continue
-                a.items = item_base + 4 * start
-                a.n_items = count
-                ev = self._event_pair(events)
-                if kid == self._stream_kernel_id():
-                    sched, n_waves, n_ctas, sync, n_groups = side.coop
-                    _lib.check(_lib.load().klnmf_solve_coop(ctypes.byref(a), sched.data_ptr(), n_waves, n_ctas,
-                                                            sync.data_ptr(), n_groups, self.stream_ptr),
-                               "klnmf_solve_coop")
-                else:
-                    _lib.check(_lib.load().klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr),
-                               "klnmf_solve_fast")
-                if ev is not None:
-                    ev[1].record(torch.cuda.current_stream(self.dev))
-                    events.append((which, kid, ev[0], ev[1]))
-            self.t_current = "csc" if which == "F" else "csr"
-        else:
-            for _, start, count in side.buckets:
-                if count == 0:
-                    continue
-                a.items = item_base + 4 * start
-                a.n_items = count
-                ev = self._event_pair(events)
-                _lib.check(_lib.load().klnmf_solve_exact(ctypes.byref(a), self.stream_ptr),
-                           "klnmf_solve_exact")
-                if ev is not None:
-                    ev[1].record(torch.cuda.current_stream(self.dev))
-                    events.append((which, -1, ev[0], ev[1]))
-        self.order[which] = np.asarray(out_order, dtype=np.int64).copy()
-        if self.world > 1:
-            self._exchange(which)
+        item_base = side.items.data_ptr()
+        lib = _lib.load()
+        for kid, start, count in side.buckets:
+            if count == 0:
+                continue
+            a.items = item_base + 4 * start
+            a.n_items = count
+            ev = self._event_pair(events)
+            if not self.fp32:
+                _lib.check(lib.klnmf_solve_exact(ctypes.byref(a), self.stream_ptr), "klnmf_solve_exact")
+            elif kid == self._stream_kernel_id():
+                sched, n_waves, n_ctas, sync, n_groups = side.coop
+                _lib.check(lib.klnmf_solve_coop(ctypes.byref(a), sched.data_ptr(), n_waves, n_ctas,
+                                                sync.data_ptr(), n_groups, self.stream_ptr), "klnmf_solve_coop")
+            else:
+                _lib.check(lib.klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr), "klnmf_solve_fast")
+            if ev is not None:
+                self._record(ev[1])
+                events.append((which, kid if self.fp32 else -1, ev[0], ev[1]))
 
     def _event_pair(self, events):
         if events is None:
             return None
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(torch.cuda.current_stream(self.dev))
+        self._record(e0)
         return e0, e1
+
+    def _record(self, ev: torch.cuda.Event) -> None:
+        """Record on the launch stream; inside a graph capture as an external
+        (timing-capable) event node."""
+        if self._capturing:
+            ev.record(torch.cuda.current_stream(self.dev))  # creates the event handle
+            _lib.call("klnmf_event_record", ev.cuda_event, self.stream_ptr, 1)
+        else:
+            ev.record(torch.cuda.current_stream(self.dev))
 
     def _exchange(self, which: str) -> None:
         """All-gather the updated rows of the moving factor (and, in fp32
