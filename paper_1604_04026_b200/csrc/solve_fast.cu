@@ -122,8 +122,11 @@ __device__ __forceinline__ void entry_init(double tq, float v, double eps, doubl
     z = u * ri;
 }
 
-// Move of the visited coordinate by delta at an entry with a != 0; the clamp
-// at 0 is the reference's (_kernels.py:105-106).
+// Move of the visited coordinate by delta; the clamp at 0 is the reference's
+// (_kernels.py:105-106).  Applied branch-free to every entry: at a == 0 it
+// reproduces t, u and z bit for bit (fma(delta, 0, t) == t and u, z are
+// recomputed from the same t by the same formula), so the reference's
+// a != 0 test is implicit.
 __device__ __forceinline__ void entry_update(double delta, double av, float v, double eps, double &t, double &u,
                                              double &z) {
     entry_init(fmax(fma(delta, av, t), 0.0), v, eps, t, u, z);
@@ -141,13 +144,35 @@ __device__ __forceinline__ void accum(double &g, double &h, double u, double z, 
     }
 }
 
-// Partials of the chunk's coordinates cc..C-1 from one entry's 16-byte chunk.
+// Partials of the chunk's coordinates cc..C-1 from one entry's 16-byte chunk
+// (runtime cc; the eps_div == 0 path).
 template <bool GUARD>
 __device__ __forceinline__ void accum_chunk(double (&red)[NV], const float4 &a4, double u, double z, int cc) {
     if (cc <= 0) accum<GUARD>(red[0], red[C + 0], u, z, (double)a4.x);
     if (cc <= 1) accum<GUARD>(red[1], red[C + 1], u, z, (double)a4.y);
     if (cc <= 2) accum<GUARD>(red[2], red[C + 2], u, z, (double)a4.z);
     accum<GUARD>(red[3], red[C + 3], u, z, (double)a4.w);
+}
+
+// Same with a compile-time first coordinate: no predication, no conversions
+// of the chunk components that are already consumed.
+template <int CC>
+__device__ __forceinline__ void accum_from(double (&red)[NV], const float4 &a4, double u, double z) {
+    if (CC <= 0) accum<false>(red[0], red[C + 0], u, z, (double)a4.x);
+    if (CC <= 1) accum<false>(red[1], red[C + 1], u, z, (double)a4.y);
+    if (CC <= 2) accum<false>(red[2], red[C + 2], u, z, (double)a4.z);
+    accum<false>(red[3], red[C + 3], u, z, (double)a4.w);
+}
+
+// Calls f(std::integral_constant<int, cc>) for a runtime cc in [0, C).
+template <typename F>
+__device__ __forceinline__ void with_cc(int cc, F &&f) {
+    switch (cc) {
+        case 0: f(std::integral_constant<int, 0>{}); break;
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        default: f(std::integral_constant<int, 3>{}); break;
+    }
 }
 
 __device__ __forceinline__ void cp_async16(unsigned smem_addr, const void *gmem, bool pred) {
@@ -305,8 +330,10 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
                 if (pm.eps_div > 0.0) {
+                    with_cc(cc, [&](auto ccv) {
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e) accum_chunk<false>(red, Ach[e * NT], u[e], z[e], cc);
+                        for (int e = 0; e < NPL; ++e) accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], z[e]);
+                    });
                 } else {
 #pragma unroll
                     for (int e = 0; e < NPL; ++e) accum_chunk<true>(red, Ach[e * NT], u[e], z[e], cc);
@@ -330,15 +357,20 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 if (delta != 0.0) {
                     moved = true;
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e) {
-                        const double av = (double)comp(Ach + e * NT, cc);
-                        if (av != 0.0) entry_update(delta, av, v[e], pm.eps_div, t[e], u[e], z[e]);
-                    }
+                    for (int e = 0; e < NPL; ++e)
+                        entry_update(delta, (double)comp(Ach + e * NT, cc), v[e], pm.eps_div, t[e], u[e], z[e]);
                 }
                 if (__any_sync(FULL_MASK, again)) {
                     double g2 = 0.0, h2 = 0.0;
+                    if (pm.eps_div > 0.0) {
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e) accum<true>(g2, h2, u[e], z[e], (double)comp(Ach + e * NT, cc));
+                        for (int e = 0; e < NPL; ++e)
+                            accum<false>(g2, h2, u[e], z[e], (double)comp(Ach + e * NT, cc));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < NPL; ++e)
+                            accum<true>(g2, h2, u[e], z[e], (double)comp(Ach + e * NT, cc));
+                    }
 #pragma unroll
                     for (int o = L / 2; o > 0; o >>= 1) {
                         g2 += __shfl_xor_sync(FULL_MASK, g2, o);
@@ -460,8 +492,10 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
                 if (pm.eps_div > 0.0) {
+                    with_cc(cc, [&](auto ccv) {
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e) accum_chunk<false>(red, Ach[e * NT], u[e], z[e], cc);
+                        for (int e = 0; e < NPL; ++e) accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], z[e]);
+                    });
                 } else {
 #pragma unroll
                     for (int e = 0; e < NPL; ++e) accum_chunk<true>(red, Ach[e * NT], u[e], z[e], cc);
@@ -484,18 +518,22 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                 if (delta != 0.0) {
                     moved = true;
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e) {
-                        const double av = (double)comp(Ach + e * NT, cc);
-                        if (av != 0.0) entry_update(delta, av, v[e], pm.eps_div, t[e], u[e], z[e]);
-                    }
+                    for (int e = 0; e < NPL; ++e)
+                        entry_update(delta, (double)comp(Ach + e * NT, cc), v[e], pm.eps_div, t[e], u[e], z[e]);
                 }
                 if (again) {
                     double ev[NV];
 #pragma unroll
                     for (int i = 0; i < NV; ++i) ev[i] = 0.0;
+                    if (pm.eps_div > 0.0) {
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e)
-                        accum<true>(ev[0], ev[1], u[e], z[e], (double)comp(Ach + e * NT, cc));
+                        for (int e = 0; e < NPL; ++e)
+                            accum<false>(ev[0], ev[1], u[e], z[e], (double)comp(Ach + e * NT, cc));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < NPL; ++e)
+                            accum<true>(ev[0], ev[1], u[e], z[e], (double)comp(Ach + e * NT, cc));
+                    }
                     bs.reduce(ev, buf);
                     g = (base + pm.alpha * x) - bs.get(buf, 0);
                     h = pm.alpha + bs.get(buf, 1);
@@ -720,19 +758,28 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                auto pass = [&](auto guard) {
-                    constexpr bool GU = decltype(guard)::value;
+                if (eps > 0.0) {
+                    with_cc(cc, [&](auto ccv) {
+                        constexpr int CC = decltype(ccv)::value;
 #pragma unroll
-                    for (int e = 0; e < NR; ++e) accum_chunk<GU>(red, A[e * NT], u[e], z[e], cc);
+                        for (int e = 0; e < NR; ++e) accum_from<CC>(red, A[e * NT], u[e], z[e]);
+#pragma unroll
+                        for (int e = 0; e < NS; ++e)
+                            accum_from<CC>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid]);
+                    });
+                    for (int64_t i = spill0 + tid; i < cn; i += NT)
+                        accum_chunk<false>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i],
+                                           Zg[i], cc);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < NR; ++e) accum_chunk<true>(red, A[e * NT], u[e], z[e], cc);
 #pragma unroll
                     for (int e = 0; e < NS; ++e)
-                        accum_chunk<GU>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid], cc);
+                        accum_chunk<true>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid], cc);
                     for (int64_t i = spill0 + tid; i < cn; i += NT)
-                        accum_chunk<GU>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i],
-                                        Zg[i], cc);
-                };
-                if (eps > 0.0) pass(std::false_type{});
-                else pass(std::true_type{});
+                        accum_chunk<true>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i],
+                                          Zg[i], cc);
+                }
                 reduce(red, buf);
                 cur = buf;
                 buf ^= 1;
@@ -753,14 +800,13 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                 for (int i = 0; i < NV; ++i) ev[i] = 0.0;
                 // apply the move (and, if the loop continues, re-evaluate this coordinate)
                 if (delta != 0.0 || again) {
-                    if (delta != 0.0) moved = true;
+                    const bool upd = delta != 0.0;  // uniform over the group
+                    if (upd) moved = true;
 #pragma unroll
-                    for (int e = 0; e < NR; ++e) {
+                    for (int e = 0; e < NR; ++e) {  // register entries: branch-free
                         const double av = (double)comp(A + e * NT, cc);
-                        if (av != 0.0) {
-                            if (delta != 0.0) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
-                            accum<false>(ev[0], ev[1], u[e], z[e], av);
-                        }
+                        if (upd) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
+                        if (eps > 0.0 || av != 0.0) accum<false>(ev[0], ev[1], u[e], z[e], av);
                     }
 #pragma unroll
                     for (int e = 0; e < NS; ++e) {
