@@ -303,6 +303,7 @@ def run_ours(args):
 
     plan.take_stats()
     step_ms = []
+    step_kernel_ms = []
     with ClockSampler(-1 if args.no_clocks else local) as clocks:
         for _ in range(args.steps):
             if not args.no_flush:
@@ -310,6 +311,10 @@ def run_ours(args):
             ev = None if args.no_kernel_events else []
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            # ~1 ms device sleep outside [e0, e1]: the host enqueues the whole
+            # step before the device reaches e0, so host latency after the
+            # per-step synchronize is not counted as device time
+            torch.cuda._sleep(2_000_000)
             e0.record(stream)
             step(ev)
             e1.record(stream)
@@ -317,9 +322,14 @@ def run_ours(args):
             # read them before the next step (device time is unaffected)
             torch.cuda.synchronize(dev)
             step_ms.append(e0.elapsed_time(e1))
+            ksum = 0.0
             for (side, kid, a, b) in ev or []:
-                kernel_ms.setdefault((side, kid), []).append(a.elapsed_time(b))
+                kms = a.elapsed_time(b)
+                ksum += kms
+                kernel_ms.setdefault((side, kid), []).append(kms)
                 launch_count[0] += 1
+            if ev:
+                step_kernel_ms.append(ksum)
     launch_count[0] += plan.aux_launches_per_step * args.steps
     st = plan.take_stats()
     total_ms = float(np.sum(step_ms))
@@ -389,6 +399,8 @@ def run_ours(args):
                                       / ((spec.n + spec.m) * r),
                                       "cap_hits": st.cap_hits, "degenerate": st.degenerate},
             "gpu_launches": launch_count[0],
+            "step_ms": [round(x, 3) for x in step_ms],
+            "step_kernel_ms": [round(x, 3) for x in step_kernel_ms] if step_kernel_ms else None,
             "clocks": clocks.summary(),
         }
 

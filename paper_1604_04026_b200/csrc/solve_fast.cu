@@ -568,6 +568,8 @@ namespace cg = cooperative_groups;
 
 constexpr int CL_NT = 512, CL_NR = 8, CL_NS = 4;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
+constexpr int CL_MAXG = 256;          // most CTAs in one cooperative row group
+constexpr size_t COOP_GROUP_BYTES = 128 + 2 * CL_MAXG * NV * sizeof(double);
 
 struct GroupRed {
     double wred[2][CL_NT / 32][NV];
@@ -591,7 +593,16 @@ __device__ __forceinline__ void cta_partial(double (&v)[NV], GroupRed &R, int bu
     }
 }
 
-// Sum over the k CTAs of a cluster through DSMEM, fixed CTA order.
+// Fixed-order warp sum (butterfly); every lane gets the total.
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    return s;
+}
+
+// Sum over the k CTAs of a cluster through DSMEM: warp i (< NV) reduces value
+// i, lane c reading CTA c's partial, so the k remote loads are in flight at
+// once; the butterfly fixes the summation order.
 struct ClusterReducer {
     GroupRed &R;
     cg::cluster_group &cl;
@@ -601,10 +612,9 @@ struct ClusterReducer {
         cta_partial(v, R, buf);
         if (k > 1) {
             cl.sync();
-            if (w == 0 && lane < NV) {
-                double s = 0.0;
-                for (int c = 0; c < k; ++c) s += cl.map_shared_rank(&R.cpart[buf][0], c)[lane];
-                R.tot[buf][lane] = s;
+            if (w < NV) {
+                const double s = warp_sum(lane < k ? cl.map_shared_rank(&R.cpart[buf][0], lane)[w] : 0.0);
+                if (lane == 0) R.tot[buf][w] = s;
             }
         } else if (w == 0 && lane < NV) {
             R.tot[buf][lane] = R.cpart[buf][lane];
@@ -624,36 +634,42 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 // for the round's G arrivals.
 struct CoopReducer {
     GroupRed &R;
-    double *slots;      // [2][G][NV], double-buffered by round parity
+    double *slots;      // [2][NV][CL_MAXG], double-buffered by round parity
     unsigned *counter;  // arrivals, G per round
     int G, rank;
     unsigned round;
     __device__ __forceinline__ void operator()(double (&v)[NV], int buf) {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         cta_partial(v, R, buf);
+        if (G == 1) {
+            if (w == 0 && lane < NV) R.tot[buf][lane] = R.cpart[buf][lane];
+            __syncthreads();
+            return;
+        }
+        // slot layout [round parity][value][CTA]: value i of all CTAs is contiguous
+        double *cur = slots + (size_t)(round & 1) * CL_MAXG * NV;
         if (w == 0) {
-            if (G > 1) {
-                double *cur = slots + (size_t)(round & 1) * G * NV;
-                if (lane < NV) {
-                    __stcg(cur + (size_t)rank * NV + lane, R.cpart[buf][lane]);
-                    __threadfence();
-                }
-                __syncwarp();
-                const unsigned target = (unsigned)G * (round + 1);
-                if (lane == 0) {
-                    atomicAdd(counter, 1u);
-                    while (ld_acquire(counter) < target) __nanosleep(64);
-                }
-                __syncwarp();
-                if (lane < NV) {
-                    (void)ld_acquire(counter);
-                    double s = 0.0;
-                    for (int c = 0; c < G; ++c) s += __ldcg(cur + (size_t)c * NV + lane);
-                    R.tot[buf][lane] = s;
-                }
-            } else if (lane < NV) {
-                R.tot[buf][lane] = R.cpart[buf][lane];
+            if (lane < NV) {
+                __stcg(cur + (size_t)lane * CL_MAXG + rank, R.cpart[buf][lane]);
+                __threadfence();
             }
+            __syncwarp();
+            const unsigned target = (unsigned)G * (round + 1);
+            if (lane == 0) {
+                atomicAdd(counter, 1u);
+                while (ld_acquire(counter) < target) __nanosleep(32);
+            }
+        }
+        __syncthreads();
+        // lane 0 of warp 0 acquired the counter; the barrier orders these loads after it
+        if (w < NV) {  // warp i sums value i over the G CTAs, all loads in flight at once
+            const double *col = cur + (size_t)w * CL_MAXG;
+            double s = 0.0;
+#pragma unroll
+            for (int c0 = 0; c0 < CL_MAXG; c0 += 32)
+                if (c0 < G) s += (c0 + lane < G) ? __ldcg(col + c0 + lane) : 0.0;
+            s = warp_sum(s);
+            if (lane == 0) R.tot[buf][w] = s;
         }
         __syncthreads();
         ++round;
@@ -881,8 +897,6 @@ __global__ void __launch_bounds__(CL_NT, 1) solve_cluster_kernel(const klnmf_sol
 // sync: per group, a 128-byte counter line then 2*CL_MAXG*NV doubles.
 // A row group's waits only point to rows of the same or an earlier wave and
 // every CTA is resident (cooperative launch), so the schedule cannot deadlock.
-constexpr int CL_MAXG = 256;
-constexpr size_t COOP_GROUP_BYTES = 128 + 2 * CL_MAXG * NV * sizeof(double);
 
 __global__ void __launch_bounds__(CL_NT, 1) solve_coop_kernel(const klnmf_solve_args_t a, const int4 *schedule,
                                                               int n_waves, unsigned char *sync) {

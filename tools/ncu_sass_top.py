@@ -6,10 +6,13 @@ import sys
 from collections import defaultdict
 
 
-def load(path):
+def load(path, which=0):
+    """SASS rows of the which-th kernel of the report."""
     out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
-    lines = out.splitlines()
+    blocks = out.split('"Kernel Name"')[1:]
+    lines = blocks[which].splitlines()
+    print("kernel:", lines[0][:120])
     i = next(k for k, l in enumerate(lines) if l.startswith('"Address"'))
     return list(csv.DictReader(io.StringIO("\n".join(lines[i:]))))
 
@@ -21,8 +24,8 @@ def num(x):
         return 0.0
 
 
-def main(path, n=40):
-    rows = load(path)
+def main(path, n=40, which=0):
+    rows = load(path, which)
     tot = sum(num(r["Warp Stall Sampling (All Samples)"]) for r in rows)
     print(f"{len(rows)} instructions, {tot:.0f} samples")
     by_op = defaultdict(float)
@@ -56,4 +59,4 @@ def main(path, n=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
