@@ -295,8 +295,8 @@ def run_ours(args):
         plan.half_step("W", ids, ids_next, alpha=reg.alpha1, beta=reg.beta1, events=events)
         ids = ids_next
 
-    for _ in range(args.warmup):
-        step(None)
+    for _ in range(args.warmup):  # same (instrumented or not) graphs as the timed steps
+        step(None if args.no_kernel_events else [])
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()

@@ -30,6 +30,7 @@
  *                               the device layout so sampled subproblems can be
  *                               compared one by one at full problem sizes
  */
+#include <float.h>
 #include <math.h>
 #include <pthread.h>
 #include <stdint.h>
@@ -317,7 +318,13 @@ void oracle_row_sums(const double *factor, int64_t r, int64_t n, double *out) {
  * with per-entry u = v/(t+eps), z = u/(t+eps): g = sum_a + alpha*x + beta -
  * sum(u*a), h = alpha + sum(z*a*a).  The control flow is solve_column's
  * (_kernels.py:73-118) verbatim.                                            */
-static inline double round_f32(double x) { return (double)(float)x; }
+/* fp32 storage value of a non-negative coordinate; subnormals are flushed to
+ * zero (the device kernels widen stored values with integer arithmetic that
+ * is exact for zero and normal floats only). */
+static inline double round_f32(double x) {
+    float f = (float)x;
+    return f < FLT_MIN ? 0.0 : (double)f;
+}
 
 void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val, int64_t n_mov,
                        const float *fixed, int64_t rp, int64_t r, const double *sum_fixed,

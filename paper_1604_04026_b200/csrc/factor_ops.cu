@@ -19,7 +19,11 @@ __global__ void to_device_kernel(const double *src, int64_t r, int64_t n, const 
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / rp;
         const int tt = (int)(e - i * rp);
-        dst[e] = tt < r ? (T)src[(int64_t)order[tt] * n + i] : (T)0;
+        T x = tt < r ? (T)src[(int64_t)order[tt] * n + i] : (T)0;
+        // fp32 storage: subnormals flush to zero (the fp32 kernels widen
+        // stored values with integer arithmetic, exact for zero and normals)
+        if (sizeof(T) == 4 && x < (T)1.17549435e-38f) x = (T)0;
+        dst[e] = x;
     }
 }
 

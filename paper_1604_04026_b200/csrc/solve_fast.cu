@@ -65,6 +65,27 @@ __device__ __forceinline__ bool enters(double g, double x, double eg) {
     return (g < -eg) || (fabs(g) > eg && x > eg);  // _kernels.py:78
 }
 
+// fp32 -> fp64 of a stored factor value on the integer pipes (the F2F
+// conversion runs on the quarter-rate XU pipe).  Exact for the values the
+// fp32-mode factors can hold: non-negative and finite (DenseFactor
+// validation, sparse.py:184) and zero or normal -- subnormals are flushed to
+// zero at every store (round_store, klnmf_layout_to_device).
+__device__ __forceinline__ double widen(float f) {
+#ifdef KLNMF_WIDEN_INT
+    const unsigned b = __float_as_uint(f);
+    const unsigned hi = (b >> 3) + (b ? 0x38000000u : 0u);  // exponent rebias 127 -> 1023
+    return __hiloint2double((int)hi, (int)(b << 29));
+#else
+    return (double)f;
+#endif
+}
+
+// Rounds a non-negative coordinate to its fp32 storage value (subnormals to 0).
+__device__ __forceinline__ double round_store(double x) {
+    const float f = __double2float_rn(x);
+    return f < 1.17549435e-38f ? 0.0 : (double)f;
+}
+
 // One Newton step of the inner loop (_kernels.py:78-115), x rounded to fp32.
 // Returns the applied delta; clears `active` when the loop ends, sets `again`
 // when the loop needs a fresh gradient.
@@ -86,7 +107,7 @@ __device__ __forceinline__ double newton_step(double g, double h, double &x, int
     }
     double target = x - g / h;
     if (target < 0.0) target = 0.0;
-    const double xn = (double)__double2float_rn(target);
+    const double xn = round_store(target);
     delta = xn - x;
     const double xo = x;
     x = xn;
@@ -104,20 +125,23 @@ __device__ __forceinline__ double newton_step(double g, double h, double &x, int
 }
 
 // 1/x: MUFU approximation refined by one Newton step (relative error ~1e-14,
-// far below the fp32 storage rounding of this mode); x == 0 (only possible
-// with eps_div == 0) returns inf like the IEEE division.
+// far below the fp32 storage rounding of this mode).  ZCHK: x == 0 (only
+// possible with eps_div == 0) returns inf like the IEEE division.
+template <bool ZCHK = true>
 __device__ __forceinline__ double fast_rcp(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     const double e = fma(-x, r, 1.0);
     r = fma(r, e, r);
+    if (!ZCHK) return r;
     return x == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : r;
 }
 
 // Maintained product of an entry and its u = v/(t+eps), z = u/(t+eps).
+template <bool ZCHK = true>
 __device__ __forceinline__ void entry_init(double tq, float v, double eps, double &t, double &u, double &z) {
     t = tq;
-    const double ri = fast_rcp(tq + eps);
+    const double ri = fast_rcp<ZCHK>(tq + eps);
     u = (double)v * ri;
     z = u * ri;
 }
@@ -130,6 +154,26 @@ __device__ __forceinline__ void entry_init(double tq, float v, double eps, doubl
 __device__ __forceinline__ void entry_update(double delta, double av, float v, double eps, double &t, double &u,
                                              double &z) {
     entry_init(fmax(fma(delta, av, t), 0.0), v, eps, t, u, z);
+}
+
+// Specialised update: CLAMP = false when delta >= 0 (t, a >= 0 keep the sum
+// non-negative, so the clamp cannot fire), ZCHK = false when eps_div > 0.
+template <bool CLAMP, bool ZCHK>
+__device__ __forceinline__ void entry_update_m(double delta, double av, float v, double eps, double &t, double &u,
+                                               double &z) {
+    const double tn = fma(delta, av, t);
+    entry_init<ZCHK>(CLAMP ? fmax(tn, 0.0) : tn, v, eps, t, u, z);
+}
+
+// Calls f(CLAMP, ZCHK) as compile-time constants for a group-uniform move.
+template <typename F>
+__device__ __forceinline__ void with_update_mode(bool any_negative, double eps, F &&f) {
+    if (eps > 0.0) {
+        if (any_negative) f(std::true_type{}, std::false_type{});
+        else f(std::false_type{}, std::false_type{});
+    } else {
+        f(std::true_type{}, std::true_type{});
+    }
 }
 
 // Adds one entry's contribution to a coordinate's (g, h) partial sums.  The
@@ -148,20 +192,20 @@ __device__ __forceinline__ void accum(double &g, double &h, double u, double z, 
 // (runtime cc; the eps_div == 0 path).
 template <bool GUARD>
 __device__ __forceinline__ void accum_chunk(double (&red)[NV], const float4 &a4, double u, double z, int cc) {
-    if (cc <= 0) accum<GUARD>(red[0], red[C + 0], u, z, (double)a4.x);
-    if (cc <= 1) accum<GUARD>(red[1], red[C + 1], u, z, (double)a4.y);
-    if (cc <= 2) accum<GUARD>(red[2], red[C + 2], u, z, (double)a4.z);
-    accum<GUARD>(red[3], red[C + 3], u, z, (double)a4.w);
+    if (cc <= 0) accum<GUARD>(red[0], red[C + 0], u, z, widen(a4.x));
+    if (cc <= 1) accum<GUARD>(red[1], red[C + 1], u, z, widen(a4.y));
+    if (cc <= 2) accum<GUARD>(red[2], red[C + 2], u, z, widen(a4.z));
+    accum<GUARD>(red[3], red[C + 3], u, z, widen(a4.w));
 }
 
 // Same with a compile-time first coordinate: no predication, no conversions
 // of the chunk components that are already consumed.
 template <int CC>
 __device__ __forceinline__ void accum_from(double (&red)[NV], const float4 &a4, double u, double z) {
-    if (CC <= 0) accum<false>(red[0], red[C + 0], u, z, (double)a4.x);
-    if (CC <= 1) accum<false>(red[1], red[C + 1], u, z, (double)a4.y);
-    if (CC <= 2) accum<false>(red[2], red[C + 2], u, z, (double)a4.z);
-    accum<false>(red[3], red[C + 3], u, z, (double)a4.w);
+    if (CC <= 0) accum<false>(red[0], red[C + 0], u, z, widen(a4.x));
+    if (CC <= 1) accum<false>(red[1], red[C + 1], u, z, widen(a4.y));
+    if (CC <= 2) accum<false>(red[2], red[C + 2], u, z, widen(a4.z));
+    accum<false>(red[3], red[C + 3], u, z, widen(a4.w));
 }
 
 // Calls f(std::integral_constant<int, cc>) for a runtime cc in [0, C).
@@ -354,22 +398,26 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 bool again = false;
                 double delta = 0.0;
                 if (active) delta = newton_step(g, h, x, inner, active, again, pm, cnt);
-                if (delta != 0.0) {
-                    moved = true;
+                if (__any_sync(FULL_MASK, delta != 0.0)) {
+                    if (delta != 0.0) moved = true;
+                    // delta == 0 (groups not moving) leaves every entry bit-identical
+                    with_update_mode(__any_sync(FULL_MASK, delta < 0.0), pm.eps_div, [&](auto cl, auto zc) {
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e)
-                        entry_update(delta, (double)comp(Ach + e * NT, cc), v[e], pm.eps_div, t[e], u[e], z[e]);
+                        for (int e = 0; e < NPL; ++e)
+                            entry_update_m<decltype(cl)::value, decltype(zc)::value>(
+                                delta, widen(comp(Ach + e * NT, cc)), v[e], pm.eps_div, t[e], u[e], z[e]);
+                    });
                 }
                 if (__any_sync(FULL_MASK, again)) {
                     double g2 = 0.0, h2 = 0.0;
                     if (pm.eps_div > 0.0) {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            accum<false>(g2, h2, u[e], z[e], (double)comp(Ach + e * NT, cc));
+                            accum<false>(g2, h2, u[e], z[e], widen(comp(Ach + e * NT, cc)));
                     } else {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            accum<true>(g2, h2, u[e], z[e], (double)comp(Ach + e * NT, cc));
+                            accum<true>(g2, h2, u[e], z[e], widen(comp(Ach + e * NT, cc)));
                     }
 #pragma unroll
                     for (int o = L / 2; o > 0; o >>= 1) {
@@ -517,9 +565,12 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                 const double delta = newton_step(g, h, x, inner, active, again, pm, cnt);
                 if (delta != 0.0) {
                     moved = true;
+                    with_update_mode(delta < 0.0, pm.eps_div, [&](auto cl, auto zc) {
 #pragma unroll
-                    for (int e = 0; e < NPL; ++e)
-                        entry_update(delta, (double)comp(Ach + e * NT, cc), v[e], pm.eps_div, t[e], u[e], z[e]);
+                        for (int e = 0; e < NPL; ++e)
+                            entry_update_m<decltype(cl)::value, decltype(zc)::value>(
+                                delta, widen(comp(Ach + e * NT, cc)), v[e], pm.eps_div, t[e], u[e], z[e]);
+                    });
                 }
                 if (again) {
                     double ev[NV];
@@ -528,11 +579,11 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                     if (pm.eps_div > 0.0) {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            accum<false>(ev[0], ev[1], u[e], z[e], (double)comp(Ach + e * NT, cc));
+                            accum<false>(ev[0], ev[1], u[e], z[e], widen(comp(Ach + e * NT, cc)));
                     } else {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            accum<true>(ev[0], ev[1], u[e], z[e], (double)comp(Ach + e * NT, cc));
+                            accum<true>(ev[0], ev[1], u[e], z[e], widen(comp(Ach + e * NT, cc)));
                     }
                     bs.reduce(ev, buf);
                     g = (base + pm.alpha * x) - bs.get(buf, 0);
@@ -820,14 +871,14 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                     if (upd) moved = true;
 #pragma unroll
                     for (int e = 0; e < NR; ++e) {  // register entries: branch-free
-                        const double av = (double)comp(A + e * NT, cc);
+                        const double av = widen(comp(A + e * NT, cc));
                         if (upd) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
                         if (eps > 0.0 || av != 0.0) accum<false>(ev[0], ev[1], u[e], z[e], av);
                     }
 #pragma unroll
                     for (int e = 0; e < NS; ++e) {
                         const int si = e * NT + tid;
-                        const double av = (double)comp(A + (NR + e) * NT, cc);
+                        const double av = widen(comp(A + (NR + e) * NT, cc));
                         if (av != 0.0) {
                             double tn = Ts[si], uu = Us[si], zz = Zs[si];
                             if (delta != 0.0) {
