@@ -629,19 +629,21 @@ struct GroupRed {
 };
 
 // CTA part of a group reduction: warp transposed reduce, fixed-order sum over
-// warps into cpart[buf] (warp 0, lanes < NV).
-__device__ __forceinline__ void cta_partial(double (&v)[NV], GroupRed &R, int buf) {
+// warps.  Returns the CTA partial of value `lane` in warp 0, lanes < NV (and
+// also stores it to cpart[buf]).
+__device__ __forceinline__ double cta_partial(double (&v)[NV], GroupRed &R, int buf) {
     constexpr int NW = CL_NT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     TReduce<32>::run(v, lane);
     if ((lane & 3) == 0) R.wred[buf][w][lane >> 2] = v[0];
     __syncthreads();
+    double s = 0.0;
     if (w == 0 && lane < NV) {
-        double s = 0.0;
 #pragma unroll
         for (int q = 0; q < NW; ++q) s += R.wred[buf][q][lane];
         R.cpart[buf][lane] = s;
     }
+    return s;
 }
 
 // Fixed-order warp sum (butterfly); every lane gets the total.
@@ -651,26 +653,87 @@ __device__ __forceinline__ double warp_sum(double s) {
     return s;
 }
 
-// Sum over the k CTAs of a cluster through DSMEM: warp i (< NV) reduces value
-// i, lane c reading CTA c's partial, so the k remote loads are in flight at
-// once; the butterfly fixes the summation order.
+// --- DSMEM push primitives (sm_90+ cluster PTX) ---
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned a, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+// CTA-scope acquire: the awaited data are shared-memory bytes counted by the
+// barrier's transaction count, written before the phase can complete.
+__device__ __forceinline__ bool mbar_try(unsigned a, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// 16 bytes into a peer CTA's shared memory, completing bytes on its mbarrier.
+__device__ __forceinline__ void st_async_v2(unsigned raddr, double x, double y, unsigned rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "d"(x), "d"(y), "r"(rmbar)
+                 : "memory");
+}
+
+constexpr int CL_MAXK = 16;  // largest cluster
+// Per-CTA inbox of the cluster all-reduce: round parity x source CTA x value.
+struct ClusterInbox {
+    __align__(16) double box[2][CL_MAXK][NV];
+    __align__(8) unsigned long long mbar[2];
+};
+
+// Sum over the k CTAs of a cluster: every CTA pushes its NV partials into
+// every peer's inbox with st.async (one-way DSMEM traffic, completion counted
+// in bytes on the receiver's mbarrier) and waits only for its own inbox -- no
+// cluster-wide barrier per reduction.  The receiver sums the k partials in CTA
+// order, so the total is identical in every CTA and deterministic.
+// Reuse: round n+2 writes the parity buffer of round n; a peer can only send
+// it after receiving this CTA's round n+1 partial, which is sent after this
+// CTA has finished reading round n.
 struct ClusterReducer {
     GroupRed &R;
-    cg::cluster_group &cl;
-    int k;
+    ClusterInbox &P;
+    int k, rank;
+    unsigned round;
     __device__ __forceinline__ void operator()(double (&v)[NV], int buf) {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        cta_partial(v, R, buf);
-        if (k > 1) {
-            cl.sync();
-            if (w < NV) {
-                const double s = warp_sum(lane < k ? cl.map_shared_rank(&R.cpart[buf][0], lane)[w] : 0.0);
-                if (lane == 0) R.tot[buf][w] = s;
+        const double s = cta_partial(v, R, buf);
+        if (w == 0) {
+            if (k > 1) {
+                const int b = round & 1;
+                const unsigned mb = smem_u32(&P.mbar[b]);
+                const unsigned slot = smem_u32(&P.box[b][rank][0]);
+                const int q = lane & (NV / 2 - 1);  // value pair of this lane
+                const double x0 = __shfl_sync(FULL_MASK, s, 2 * q);
+                const double x1 = __shfl_sync(FULL_MASK, s, 2 * q + 1);
+                for (int i = lane; i < k * (NV / 2); i += 32) {
+                    const unsigned peer = (unsigned)(i / (NV / 2));
+                    st_async_v2(mapa_u32(slot + 16u * q, peer), x0, x1, mapa_u32(mb, peer));
+                }
+                if (lane == 0) mbar_arrive_tx(mb, (unsigned)(k * NV * sizeof(double)));
+                while (!mbar_try(mb, (round >> 1) & 1u)) {
+                }
+                if (lane < NV) {
+                    double t = 0.0;
+                    for (int c = 0; c < k; ++c) t += P.box[b][c][lane];
+                    R.tot[buf][lane] = t;
+                }
+            } else if (lane < NV) {
+                R.tot[buf][lane] = s;
             }
-        } else if (w == 0 && lane < NV) {
-            R.tot[buf][lane] = R.cpart[buf][lane];
         }
         __syncthreads();
+        ++round;
     }
 };
 
@@ -937,11 +1000,19 @@ __global__ void __launch_bounds__(CL_NT, 1) solve_cluster_kernel(const klnmf_sol
     if (slot >= a.n_items) return;  // uniform over the cluster
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ GroupRed R;
+    __shared__ ClusterInbox P;
     __shared__ double ssum[KMAX_RP];
     for (int kk = threadIdx.x; kk < a.r; kk += CL_NT) ssum[kk] = a.sum_pos[kk];
-    ClusterReducer red{R, cl, k};
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&P.mbar[0]), 1);
+        mbar_init(smem_u32(&P.mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (k > 1) cl.sync();  // every inbox is initialised before the first push
+    else __syncthreads();
+    ClusterReducer red{R, P, k, cq, 0u};
     solve_slice(a, slot, cq, k, red, R, smem_raw, ssum);
-    if (k > 1) cl.sync();  // peers may still read this CTA's shared memory
+    if (k > 1) cl.sync();  // no CTA exits while a peer may still address it
 }
 
 // schedule: [n_waves][gridDim.x] int4 (item slot or -1, rank, G, group id);
