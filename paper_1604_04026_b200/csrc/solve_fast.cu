@@ -617,9 +617,12 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 // moves of the chunk read it from there.
 namespace cg = cooperative_groups;
 
-constexpr int CL_NT = 512, CL_NR = 8, CL_NS = 4;
+// 256 threads and at most ~113 KB of shared memory per CTA: two slices (of
+// different rows, or of one row) share an SM, so one CTA's reduction and
+// gather latency overlaps the other's arithmetic.
+constexpr int CL_NT = 256, CL_NR = 8, CL_NS = 4, CL_PER_SM = 2;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
-constexpr int CL_MAXG = 256;          // most CTAs in one cooperative row group
+constexpr int CL_MAXG = 512;          // most CTAs in one cooperative row group
 constexpr size_t COOP_GROUP_BYTES = 128 + 2 * CL_MAXG * NV * sizeof(double);
 
 struct GroupRed {
@@ -992,7 +995,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     flush_stats(cnt, cq == 0 && tid == 0, a.stats, false);
 }
 
-__global__ void __launch_bounds__(CL_NT, 1) solve_cluster_kernel(const klnmf_solve_args_t a) {
+__global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_cluster_kernel(const klnmf_solve_args_t a) {
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.num_blocks();
     const int cq = (int)cl.block_rank();
@@ -1020,7 +1023,7 @@ __global__ void __launch_bounds__(CL_NT, 1) solve_cluster_kernel(const klnmf_sol
 // A row group's waits only point to rows of the same or an earlier wave and
 // every CTA is resident (cooperative launch), so the schedule cannot deadlock.
 
-__global__ void __launch_bounds__(CL_NT, 1) solve_coop_kernel(const klnmf_solve_args_t a, const int4 *schedule,
+__global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_coop_kernel(const klnmf_solve_args_t a, const int4 *schedule,
                                                               int n_waves, unsigned char *sync) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ GroupRed R;
@@ -1048,10 +1051,14 @@ struct FastKernel {
 #define WK(L, NPL) {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL>, 128 / (L), NPL, 0}
 #define BK(NT, NPL) {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL>, 1, NPL, 0}
 #define CK(K) {CL_NT * (K), CL_NE, CL_NT, (int64_t)(K) * CL_NT * CL_NE, solve_cluster_kernel, 1, 0, (K)}
+// Ascending capacity.  Every padding slot of a subproblem costs as much as a
+// real entry, so the ladder is dense (<= 25% steps) where the F side's and the
+// W side's subproblem sizes concentrate (SURVEY.md §8(d) size profiles).
 const FastKernel kFast[] = {
-    WK(1, 4),  WK(2, 4),  WK(4, 4),   WK(8, 4),   WK(8, 8),   WK(16, 8),
-    WK(32, 8), BK(64, 8), BK(128, 8), BK(256, 8), BK(512, 8),
-    CK(1),     CK(2),     CK(4),      CK(8),      CK(16),
+    WK(1, 4),   WK(2, 4),   WK(4, 4),   WK(8, 4),   WK(8, 6),   WK(8, 8),   WK(16, 6),  WK(16, 8),
+    WK(32, 5),  WK(32, 6),  WK(32, 7),  WK(32, 8),  BK(64, 5),  BK(64, 6),  BK(64, 7),  BK(64, 8),
+    BK(128, 5), BK(128, 6), BK(128, 7), BK(128, 8), BK(256, 6), BK(256, 8), BK(512, 6), BK(512, 8),
+    CK(2),      CK(4),      CK(8),      CK(16),
     // unbounded: the cooperative long-row kernel (klnmf_solve_coop, schedule built by the caller)
     {CL_NT, CL_NE, CL_NT, -1, nullptr, 1, 0, -1},
 };

@@ -196,13 +196,15 @@ def test_every_bucket_kernel(cuda_ok):
     import paper_1604_04026_b200 as kb
     from paper_1604_04026_b200.plan import DevicePlan
 
+    from paper_1604_04026_b200 import _lib
+
     rng = np.random.default_rng(5)
     n = 200000
-    sizes = [0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257,
-             511, 512, 513, 1023, 1024, 1025, 2047, 2048, 2049, 3000, 4095, 4097, 5999, 10240, 10241, 20000,
-             40000, 60000]
-    # 16-CTA cluster; cooperative long-row kernel (several rows per wave, multi-CTA groups)
-    sizes = sizes * 3 + [90000, 100000, 180000, 199000]
+    # both edges of every bucket of the capacity ladder; the small ones three
+    # times (several subproblems per warp / block), then cooperative long rows
+    caps = [c for _, c, _, _ in _lib.fast_kernels() if c > 0]
+    edges = sorted({c + d for c in caps for d in (-1, 0, 1)} | {0, 3000})
+    sizes = [e for e in edges if e <= 4097] * 3 + [e for e in edges if e > 4097] + [100000, 180000, 199000]
     rows, cols = [], []
     for j, s in enumerate(sizes):
         rr = np.sort(rng.choice(n, size=s, replace=False))
