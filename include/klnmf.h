@@ -53,6 +53,9 @@ extern "C" {
 
 int klnmf_abi_version(void);
 const char *klnmf_last_error(void);
+/* Counter-mode chunk order of one subproblem, computed on the host with the
+ * device's generator (uint8 order[nchunks], nchunks <= 64). */
+int klnmf_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t nchunks, uint8_t *order);
 /* Record a CUDA event on a stream; external != 0 makes a recording inside a
  * CUDA-graph capture a real (timing-capable) event node, re-recorded by every
  * replay (used for per-kernel timing of captured half-steps). */
@@ -119,7 +122,23 @@ typedef struct {
     double alpha, beta, eps_grad, eps_x, eps_div;
     int64_t inner_cap;
     unsigned long long *stats; /* device, KLNMF_STATS_LEN, accumulated */
+    /* Coordinate order inside a subproblem (fp32 mode; exact mode requires
+     * KLNMF_ORDER_SHARED).  KLNMF_ORDER_SHARED visits the storage order, i.e.
+     * the iteration's shared permutation -- the reference's ids stream
+     * (solver.py:276,287).  KLNMF_ORDER_COUNTER visits the subproblem's
+     * 4-coordinate chunks in a per-(seed, iteration, subproblem, side) order:
+     * Fisher-Yates driven by Philox4x32-10 with key (order_seed lo, hi) and
+     * counter (block, subproblem id, *order_iter, order_side); storage order
+     * inside a chunk.  order_iter is a device pointer so a captured launch
+     * sequence can be replayed for every iteration. */
+    int32_t order_mode;
+    uint32_t order_side;
+    uint64_t order_seed;
+    const uint32_t *order_iter;
 } klnmf_solve_args_t;
+
+#define KLNMF_ORDER_SHARED 0
+#define KLNMF_ORDER_COUNTER 1
 
 /* exact fp64 solver (bit-identical to _kernels.sweep_range, one warp per subproblem) */
 int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream);

@@ -321,6 +321,59 @@ void oracle_row_sums(const double *factor, int64_t r, int64_t n, double *out) {
 /* fp32 storage value of a non-negative coordinate; subnormals are flushed to
  * zero (the device kernels widen stored values with integer arithmetic that
  * is exact for zero and normal floats only). */
+/* ------------------------------------------------------------------ */
+/* Counter-based coordinate order (north-star (c)).  Not part
+ * of the reference: it replaces the reference's single ids permutation per
+ * iteration (solver.py:276,287) by an order per (seed, iteration, subproblem,
+ * side) that needs no host stream.  Generator: Philox4x32-10 (Salmon et al.,
+ * SC'11, "Parallel random numbers: as easy as 1, 2, 3"), restated from the
+ * published round function:
+ *   (hi0, lo0) = mulhilo(0xD2511F53, c0); (hi1, lo1) = mulhilo(0xCD9E8D57, c2)
+ *   c <- (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0);  k += (0x9E3779B9, 0xBB67AE85)
+ * with the key bumped between the 10 rounds.                                  */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int rnd = 0; rnd < 10; ++rnd) {
+        if (rnd > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+/* Visit order of the nchunks 4-coordinate chunks of subproblem `item`:
+ * Fisher-Yates from the top, step k = n-1-i drawing word k of the Philox
+ * stream with counter (k / 4, item, iter, side) and key (seed lo, seed hi);
+ * the index is the multiply-shift (word * (i+1)) >> 32. */
+void oracle_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t nchunks,
+                        uint8_t *order) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t words[4] = {0, 0, 0, 0};
+    for (int32_t i = 0; i < nchunks; ++i) order[i] = (uint8_t)i;
+    for (int32_t i = nchunks - 1, k = 0; i >= 1; --i, ++k) {
+        if ((k & 3) == 0) {
+            const uint32_t ctr[4] = {(uint32_t)(k >> 2), item, iter, side};
+            oracle_philox4x32_10(ctr, key, words);
+        }
+        const uint32_t j = (uint32_t)(((uint64_t)words[k & 3] * (uint32_t)(i + 1)) >> 32);
+        const uint8_t tmp = order[i];
+        order[i] = order[j];
+        order[j] = tmp;
+    }
+}
+
 static inline double round_f32(double x) {
     float f = (float)x;
     return f < FLT_MIN ? 0.0 : (double)f;
@@ -330,8 +383,11 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
                        const float *fixed, int64_t rp, int64_t r, const double *sum_fixed,
                        float *moving, double *t, const int64_t *items, int64_t n_items,
                        double alpha, double beta, double eps_grad, double eps_x, double eps_div,
-                       int64_t inner_cap, int64_t *stats) {
+                       int64_t inner_cap, int64_t *stats, int order_mode, uint64_t order_seed,
+                       uint32_t order_iter, uint32_t order_side) {
     (void)n_mov;
+    const int32_t nchunks = (int32_t)((r + 3) / 4);
+    uint8_t corder[64];
     int64_t cap_s = 0;
     for (int64_t q = 0; q < n_items; ++q) {
         int64_t j = items ? items[q] : q;
@@ -350,7 +406,12 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
             z[p] = u[p] * rinv;
         }
         stats[STAT_PASSES] += 1;
-        for (int64_t tt = 0; tt < r; ++tt) {
+        /* shared order: storage order; counter order: chunks in the
+         * subproblem's own order, storage order inside a chunk */
+        if (order_mode) oracle_chunk_order(order_seed, order_iter, (uint32_t)j, order_side, nchunks, corder);
+        for (int64_t vis = 0; vis < (order_mode ? 4 * (int64_t)nchunks : r); ++vis) {
+            const int64_t tt = order_mode ? 4 * (int64_t)corder[vis / 4] + vis % 4 : vis;
+            if (tt >= r) continue;
             double x = (double)moving[j * rp + tt];
             double g, h;
 #define EVAL()                                                            \

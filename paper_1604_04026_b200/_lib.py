@@ -25,6 +25,7 @@ EXPORTS = (
     "klnmf_abi_version",
     "klnmf_last_error",
     "klnmf_event_record",
+    "klnmf_chunk_order",
     "klnmf_sweep_range",
     "klnmf_kl_data_term",
     "klnmf_row_sums",
@@ -47,6 +48,7 @@ EXPORTS = (
 )
 
 STATS_LEN = 4
+ORDER_SHARED, ORDER_COUNTER = 0, 1
 STAT_CAP_HITS, STAT_DEGENERATE, STAT_INNER_ITERS, STAT_PASSES = range(4)
 
 
@@ -89,6 +91,10 @@ class SolveArgs(ctypes.Structure):
         ("eps_div", D),
         ("inner_cap", I64),
         ("stats", P),
+        ("order_mode", I32),
+        ("order_side", ctypes.c_uint32),
+        ("order_seed", ctypes.c_uint64),
+        ("order_iter", P),
     ]
 
 
@@ -96,6 +102,7 @@ _SIGS = {
     "klnmf_abi_version": ([], INT),
     "klnmf_last_error": ([], ctypes.c_char_p),
     "klnmf_event_record": ([P, P, INT], INT),
+    "klnmf_chunk_order": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, I32, P], INT),
     "klnmf_sweep_range": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, P], INT),
     "klnmf_kl_data_term": ([P, P, P, P, P, D, I64, I64, I64, P], INT),
     "klnmf_row_sums": ([P, I64, I64, P], INT),

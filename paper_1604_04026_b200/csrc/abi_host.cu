@@ -99,6 +99,13 @@ extern "C" int klnmf_abi_version(void) { return KLNMF_ABI_VERSION; }
 
 extern "C" const char *klnmf_last_error(void) { return g_err; }
 
+extern "C" int klnmf_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t nchunks,
+                                 uint8_t *order) {
+    if (nchunks < 0 || nchunks > klnmf::MAX_CHUNKS) return set_error_msg(1, "klnmf_chunk_order: 0 <= nchunks <= 64");
+    klnmf::chunk_order(seed, iter, item, side, nchunks, order);
+    return 0;
+}
+
 extern "C" int klnmf_event_record(void *event, void *stream, int external) {
     cudaEvent_t ev = static_cast<cudaEvent_t>(event);
     if (external)
@@ -178,7 +185,7 @@ extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx,
     rc = klnmf_layout_to_device(d_mov_ref, r, n_mov, d_order, rp, d_moving, 0, st);
     if (rc) return rc;
 
-    klnmf_solve_args_t a;
+    klnmf_solve_args_t a = {};  // shared coordinate order (the reference ids)
     memset(&a, 0, sizeof(a));
     a.side.ptr = d_ptr;
     a.side.idx = d_idx;

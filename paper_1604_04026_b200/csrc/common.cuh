@@ -32,6 +32,50 @@ cudaError_t ensure_smem(const void *fn, size_t bytes);
 
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): one 128-bit block of the
+// counter c under key (k0, k1); the published round function, key bumped
+// between rounds.  Shared by the kernels and the host (klnmf_chunk_order).
+__host__ __device__ inline void philox4x32_10(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+    for (int rnd = 0; rnd < 10; ++rnd) {
+        if (rnd > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c[0] = hi1 ^ c[1] ^ k0;
+        c[1] = lo1;
+        c[2] = hi0 ^ c[3] ^ k1;
+        c[3] = lo0;
+    }
+}
+
+constexpr int MAX_CHUNKS = 64;  // 4-coordinate chunks of the largest padded rank (256)
+
+// Counter-mode visit order of a subproblem's n 4-coordinate chunks:
+// Fisher-Yates from the top, step k = n-1-i using word k of the Philox stream
+// (counter (k/4, item, iter, side), key (seed lo, seed hi)), index
+// (word * (i+1)) >> 32.  Identical on host and device.
+__host__ __device__ inline void chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int n,
+                                            uint8_t *order) {
+    for (int i = 0; i < n; ++i) order[i] = (uint8_t)i;
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int i = n - 1, k = 0; i >= 1; --i, ++k) {
+        if ((k & 3) == 0) {
+            w[0] = (uint32_t)(k >> 2);
+            w[1] = item;
+            w[2] = iter;
+            w[3] = side;
+            philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
+        }
+        const uint32_t j = (uint32_t)(((uint64_t)w[k & 3] * (uint32_t)(i + 1)) >> 32);
+        const uint8_t tmp = order[i];
+        order[i] = order[j];
+        order[j] = tmp;
+    }
+}
+
 __device__ __forceinline__ float4 ldg_f4(const float *p) {
     return __ldg(reinterpret_cast<const float4 *>(p));
 }

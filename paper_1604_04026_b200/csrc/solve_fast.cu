@@ -300,6 +300,8 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);                 // [STAGES][NPL][NT]
     float *xs_all = reinterpret_cast<float *>(ring + STAGES * NPL * NT);  // [GPB][2][rps]
+    // counter order only: [GPB][MAX_CHUNKS] visit order of each group's chunks
+    uint8_t *cord_all = reinterpret_cast<uint8_t *>(xs_all + GPB * 2 * (a.rp | 1));
     __shared__ double ssum[KMAX_RP];  // fixed-factor row sums by position
     __shared__ double tots[GPB][NV];  // reduced partial sums of each group
 
@@ -327,6 +329,11 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     const int s = valid ? (int)(a.side.ptr[j + 1] - lo) : 0;
 
     for (int k = gl; k < r; k += L) xs[k] = valid ? moving[j * rp + a.perm_in[k]] : 0.f;
+    const int nchunks = (r + C - 1) / C;
+    const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
+    uint8_t *cord = cord_all + grp * MAX_CHUNKS;
+    if (counter && gl == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
+    __syncwarp();
 
     double t[NPL], u[NPL], z[NPL];
     float v[NPL];
@@ -346,12 +353,13 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
         }
     }
     const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * tid;
-    const int nchunks = (r + C - 1) / C;
+    auto phys = [&](int chunk) -> int { return counter ? (int)cord[chunk] : chunk; };
     auto issue = [&](int chunk) {
         if (chunk < nchunks) {
             const unsigned base = ring_s + 16u * NT * NPL * (chunk % STAGES);
+            const int pc = phys(chunk);
 #pragma unroll
-            for (int e = 0; e < NPL; ++e) cp_async16(base + 16u * NT * e, row[e] + chunk * C, gl + e * L < s);
+            for (int e = 0; e < NPL; ++e) cp_async16(base + 16u * NT * e, row[e] + pc * C, gl + e * L < s);
         }
         cp_commit();
     };
@@ -364,11 +372,13 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
         issue(ch + STAGES - 1);
         cp_wait<STAGES - 1>();
         const float4 *Ach = ring + (ch % STAGES) * NPL * NT + tid;  // own slots of this stage
-        const int nc = min(C, r - ch * C);
+        const int pc = phys(ch);  // per group in counter order
+        const int nc = counter ? C : min(C, r - ch * C);
         bool fresh = false;  // tot valid for the current t
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
-            const int tt = ch * C + cc;
+            const int tt = pc * C + cc;
+            const bool live = tt < r;
             if (__any_sync(FULL_MASK, !fresh)) {
                 double red[NV];
 #pragma unroll
@@ -392,7 +402,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
             double g = (base + pm.alpha * x) - tot[cc];
             double h = pm.alpha + tot[C + cc];
             int inner = 0;
-            bool active = valid && enters(g, x, pm.eps_grad);
+            bool active = valid && live && enters(g, x, pm.eps_grad);
             bool moved = false;
             while (__any_sync(FULL_MASK, active)) {
                 bool again = false;
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 }
             }
             if (moved) fresh = false;
-            if (gl == 0 && valid) xo[tt] = (float)x;
+            if (gl == 0 && valid && live) xo[tt] = (float)x;
         }
     }
     cp_wait<0>();
@@ -475,6 +485,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);             // [STAGES][NPL][NT]
     float *xs = reinterpret_cast<float *>(ring + STAGES * NPL * NT);  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
+    uint8_t *cord = reinterpret_cast<uint8_t *>(xo + (a.rp | 1));  // counter order only
     __shared__ double ssum[KMAX_RP];
     __shared__ BlockSums<NT> bs;
 
@@ -512,11 +523,18 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     }
     const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
+    const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
+    if (counter) {
+        if (tid == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
+        __syncthreads();
+    }
+    auto phys = [&](int chunk) -> int { return counter ? (int)cord[chunk] : chunk; };
     auto issue = [&](int chunk) {
         if (chunk < nchunks) {
             const unsigned base = ring_s + 16u * NT * NPL * (chunk % STAGES);
+            const int pc = phys(chunk);
 #pragma unroll
-            for (int e = 0; e < NPL; ++e) cp_async16(base + 16u * NT * e, row[e] + chunk * C, tid + e * NT < s);
+            for (int e = 0; e < NPL; ++e) cp_async16(base + 16u * NT * e, row[e] + pc * C, tid + e * NT < s);
         }
         cp_commit();
     };
@@ -530,11 +548,12 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
         issue(ch + STAGES - 1);
         cp_wait<STAGES - 1>();
         const float4 *Ach = ring + (ch % STAGES) * NPL * NT + tid;
-        const int nc = min(C, r - ch * C);
+        const int pc = phys(ch);
+        const int nc = min(C, r - pc * C);
         bool fresh = false;
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
-            const int tt = ch * C + cc;
+            const int tt = pc * C + cc;
             if (!fresh) {  // block-uniform
                 double red[NV];
 #pragma unroll
@@ -805,6 +824,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     int2 *VO = reinterpret_cast<int2 *>(Zs + NS * NT);    // (float bits of v, row offset)
     float *xs = reinterpret_cast<float *>(VO + NS * NT);  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
+    uint8_t *cord = reinterpret_cast<uint8_t *>(xo + (a.rp | 1));  // counter order
 
     const Params pm(a);
     const int tid = threadIdx.x;
@@ -866,27 +886,30 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, Tg[i], Ug[i], Zg[i]);
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
+    const int nchunks = (r + C - 1) / C;
+    const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
+    if (counter && tid == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
     __syncthreads();
 
     Counters cnt;
     int buf = 0, cur = 0;
-    const int nchunks = (r + C - 1) / C;
     for (int ch = 0; ch < nchunks; ++ch) {
+        const int pc = counter ? (int)cord[ch] : ch;  // physical chunk
         // gather this chunk of every resident entry once (own slots only)
 #pragma unroll
         for (int e = 0; e < NR; ++e)
-            cp_async16(cache_s + 16u * NT * e, fixed + max(off[e], 0) + ch * C, off[e] >= 0);
+            cp_async16(cache_s + 16u * NT * e, fixed + max(off[e], 0) + pc * C, off[e] >= 0);
 #pragma unroll
         for (int e = 0; e < NS; ++e)
-            cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + ch * C, offs[e] >= 0);
+            cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + pc * C, offs[e] >= 0);
         cp_commit();
         cp_wait<0>();
         const float4 *A = cache + tid;
-        const int nc = min(C, r - ch * C);
+        const int nc = min(C, r - pc * C);
         bool fresh = false;
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
-            const int tt = ch * C + cc;
+            const int tt = pc * C + cc;
             if (!fresh) {  // uniform over the group
                 double red[NV];
 #pragma unroll
@@ -901,7 +924,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                             accum_from<CC>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid]);
                     });
                     for (int64_t i = spill0 + tid; i < cn; i += NT)
-                        accum_chunk<false>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i],
+                        accum_chunk<false>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), Ug[i],
                                            Zg[i], cc);
                 } else {
 #pragma unroll
@@ -910,7 +933,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                     for (int e = 0; e < NS; ++e)
                         accum_chunk<true>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid], cc);
                     for (int64_t i = spill0 + tid; i < cn; i += NT)
-                        accum_chunk<true>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + ch * C), Ug[i],
+                        accum_chunk<true>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), Ug[i],
                                           Zg[i], cc);
                 }
                 reduce(red, buf);
@@ -1069,7 +1092,7 @@ constexpr int kNumFast = sizeof(kFast) / sizeof(kFast[0]);
 
 inline size_t slice_smem(int rp) {
     return (size_t)CL_NE * CL_NT * sizeof(float4) + (size_t)CL_NS * CL_NT * (3 * sizeof(double) + sizeof(int2)) +
-           2 * sizeof(float) * (size_t)(rp | 1) + 16;
+           2 * sizeof(float) * (size_t)(rp | 1) + MAX_CHUNKS + 16;
 }
 
 }  // namespace
@@ -1092,6 +1115,8 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (args->n_items <= 0) return 0;
     if (args->rp % 4 != 0) return set_error_msg(1, "klnmf_solve_fast: rp must be a multiple of 4");
     if (args->rp > KMAX_RP) return set_error_msg(1, "klnmf_solve_fast: rank above 256 is not supported in fp32 mode");
+    if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
+        return set_error_msg(1, "klnmf_solve_fast: bad coordinate order mode");
     const FastKernel &k = kFast[kernel_id];
     if (k.cluster < 0) return set_error_msg(1, "klnmf_solve_fast: the long-row bucket runs through klnmf_solve_coop");
     if (k.cluster > 0) {
@@ -1122,7 +1147,8 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     }
     const int64_t blocks = (args->n_items + k.gpb - 1) / k.gpb;
     const size_t ring = sizeof(float4) * (size_t)STAGES * (size_t)k.ring_entries * (size_t)k.nt;
-    const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) + 16;
+    const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) +
+                        (args->order_mode != KLNMF_ORDER_SHARED ? (size_t)k.gpb * MAX_CHUNKS : 0) + 16;
     if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
     k.fn<<<(unsigned)blocks, k.nt, smem, as_stream(stream)>>>(*args);
     KLNMF_CHECK_LAUNCH("klnmf_solve_fast");
@@ -1147,6 +1173,8 @@ extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *sche
     if (n_waves <= 0 || args->n_items <= 0) return 0;
     if (args->rp > KMAX_RP) return set_error_msg(1, "klnmf_solve_coop: rank above 256 is not supported");
     if (args->scratch == nullptr) return set_error_msg(1, "klnmf_solve_coop: needs a scratch buffer");
+    if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
+        return set_error_msg(1, "klnmf_solve_coop: bad coordinate order mode");
     cudaStream_t st = as_stream(stream);
     const size_t smem = slice_smem(args->rp);
     KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, smem));

@@ -88,9 +88,15 @@ class SidePlan:
 
 class DevicePlan:
     def __init__(self, V, rank: int, precision: str = "fp64", device=None, group=None,
-                 ledger=None, fast_kernels: list | None = None):
+                 ledger=None, fast_kernels: list | None = None, order: str = "shared", order_seed: int = 0):
         if precision not in ("fp64", "fp32"):
             raise ValueError("precision must be 'fp64' or 'fp32'")
+        if order not in ("shared", "counter"):
+            raise ValueError("order must be 'shared' or 'counter'")
+        if order == "counter" and precision != "fp32":
+            raise ValueError("the counter coordinate order is an fp32-mode option (fp64 is the oracle mode)")
+        self.order_mode = _lib.ORDER_COUNTER if order == "counter" else _lib.ORDER_SHARED
+        self.order_seed = int(order_seed) & (2**64 - 1)
         if not torch.cuda.is_available():
             raise RuntimeError("DevicePlan needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -171,8 +177,9 @@ class DevicePlan:
             self.t_current = None  # which maintained-product array is valid ("csc"/"csr")
             self.stats = torch.zeros(_lib.STATS_LEN, dtype=torch.int64, device=dev)
             self.sum_pos = torch.zeros(self.rp, dtype=torch.float64, device=dev)
-            self._perm = torch.zeros(3, self.rp, dtype=torch.int32, device=dev)
-            self._perm_host = torch.zeros(3, self.rp, dtype=torch.int32).pin_memory()
+            # rows: perm_in, perm_out, nat_pos, [iteration counter of the counter order]
+            self._perm = torch.zeros(4, self.rp, dtype=torch.int32, device=dev)
+            self._perm_host = torch.zeros(4, self.rp, dtype=torch.int32).pin_memory()
             self._perm_event = None
             self.use_graphs = True
             self._capturing = False
@@ -322,7 +329,7 @@ class DevicePlan:
 
     def half_step(self, which: str, ids, ids_next=None, alpha: float = 0.0, beta: float = 0.0,
                   tol: Tolerances = Tolerances(), sums_pos: np.ndarray | None = None,
-                  events: list | None = None) -> None:
+                  events: list | None = None, iteration: int | None = None) -> None:
         """Solve every subproblem of one side (which="F": columns, W fixed;
         which="W": rows, F fixed) in place, visiting coordinates in `ids`.
 
@@ -338,7 +345,13 @@ class DevicePlan:
         the contents of the visit-order maps (and the row sums) change.  The
         launch sequence of each side is therefore captured once into a CUDA
         graph and replayed, the maps arriving by an asynchronous pinned copy.
+
+        With the counter coordinate order (plan order="counter") `iteration`
+        is the counter of the per-subproblem chunk orders (it travels with the
+        maps, so the captured graphs stay valid).
         """
+        if self.order_mode == _lib.ORDER_COUNTER and iteration is None:
+            raise ValueError("the counter coordinate order needs the iteration number")
         ids = np.asarray(ids, dtype=np.int64)
         fixed_name = "W" if which == "F" else "F"
         if self.order[fixed_name] is None or not np.array_equal(self.order[fixed_name], ids):
@@ -348,7 +361,10 @@ class DevicePlan:
         perm_in = np.argsort(o_mov)[ids]
         perm_out = np.argsort(out_order)[ids]
         nat_pos = np.argsort(ids)
-        self._stage_perms(np.stack([self._padded(perm_in), self._padded(perm_out), self._padded(nat_pos)]))
+        it_row = np.zeros(self.rp, dtype=np.int64)
+        it_row[0] = 0 if iteration is None else int(iteration) & 0xFFFFFFFF
+        self._stage_perms(np.stack([self._padded(perm_in), self._padded(perm_out), self._padded(nat_pos),
+                                    it_row.astype(np.uint32).view(np.int32)]))
         dev_sums = sums_pos is None
         if not dev_sums:
             sp = np.zeros(self.rp)
@@ -437,6 +453,10 @@ class DevicePlan:
         a.inner_cap = int(tol.inner_iter_cap)
         a.stats = self.stats.data_ptr()
         a.scratch = self.scratch.data_ptr()
+        a.order_mode = self.order_mode
+        a.order_side = 0 if which == "F" else 1
+        a.order_seed = self.order_seed
+        a.order_iter = self._perm[3].data_ptr()
         if self.fp32:
             need = "csr" if which == "F" else "csc"
             a.tmap = side.tmap.data_ptr()

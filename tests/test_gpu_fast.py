@@ -133,8 +133,9 @@ def _device_state(plan, which):
     return ptr, idx, val, fixed, moving, t_in[tmap]
 
 
-def _compare_half_step(plan, which, ids, alpha, beta):
-    """Run one half-step on the GPU and on the fp32 oracle from the same state."""
+def _compare_half_step(plan, which, ids, alpha, beta, iteration=None):
+    """Run one half-step on the GPU and on the fp32 oracle from the same state
+    (counter-order plans: chunk orders of `iteration`)."""
     import torch
 
     fixed_name = "W" if which == "F" else "F"
@@ -142,8 +143,12 @@ def _compare_half_step(plan, which, ids, alpha, beta):
     sums = plan.row_sums_pos(fixed_name, torch.zeros(plan.rp, dtype=torch.float64, device=plan.dev)).cpu().numpy()
     mov_or = moving.copy()
     t_or = t0.copy()
-    st_or = oracle.sweep_fp32(ptr, idx, val, fixed, plan.rp, plan.r, sums, mov_or, t_or, None, alpha, beta)
-    plan.half_step(which, ids, alpha=alpha, beta=beta)
+    order = None
+    if plan.order_mode != 0:
+        order = (plan.order_seed, iteration, 0 if which == "F" else 1)
+    st_or = oracle.sweep_fp32(ptr, idx, val, fixed, plan.rp, plan.r, sums, mov_or, t_or, None, alpha, beta,
+                              order=order)
+    plan.half_step(which, ids, alpha=alpha, beta=beta, iteration=iteration)
     st_gpu = plan.take_stats()
     mov_gpu = plan.factors[which].cpu().numpy()
     t_gpu = plan.t["csc" if which == "F" else "csr"].cpu().numpy()[: plan.nnz]
@@ -188,6 +193,86 @@ def test_half_step_vs_fp32_oracle(cuda_ok, name):
         mg, mo, tg, to, sg, so = _compare_half_step(plan, which, ids, a, b)
         _check(mg, mo, tg, to, f"{name} {which}")
         _check_stats(sg, so)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_counter_order_half_step_vs_fp32_oracle(cuda_ok, name):
+    """Counter-based per-subproblem chunk order (north-star (c)): every bucket
+    kernel draws the same Philox orders as the oracle's restatement."""
+    from paper_1604_04026_b200 import synth
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    spec = _spec(name)
+    if name == "C4":
+        spec = spec.scaled(m=8000)
+    V = synth.generate(spec)
+    w0, f0 = synth.initial_factors(spec)
+    plan = DevicePlan(V, spec.rank, "fp32", order="counter", order_seed=spec.seed + 11)
+    ids = np.random.default_rng(0).permutation(spec.rank)
+    plan.set_factors(w0, f0, order=ids)
+    for it in (1, 7):
+        for which, a, b in (("F", spec.reg.alpha2, spec.reg.beta2), ("W", spec.reg.alpha1, spec.reg.beta1)):
+            mg, mo, tg, to, sg, so = _compare_half_step(plan, which, ids, a, b, iteration=it)
+            _check(mg, mo, tg, to, f"{name} counter it{it} {which}")
+            _check_stats(sg, so)
+
+
+def test_counter_order_every_bucket_and_rank_padding(cuda_ok):
+    """Counter order with r % 4 != 0 (a partial last chunk visited anywhere in
+    the order) on subproblems of every bucket."""
+    import paper_1604_04026_b200 as kb
+    from paper_1604_04026_b200 import _lib
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    rng = np.random.default_rng(9)
+    n = 120000
+    caps = [c for _, c, _, _ in _lib.fast_kernels() if c > 0]
+    sizes = [c for c in caps if c <= 49152] + [0, 1, 77, 60000, 110000]
+    rows, cols = [], []
+    for j, s_ in enumerate(sizes):
+        rows.append(np.sort(rng.choice(n, size=s_, replace=False)))
+        cols.append(np.full(s_, j))
+    V = kb.SparseMatrix.from_coo(n, len(sizes), np.concatenate(rows), np.concatenate(cols),
+                                 rng.integers(1, 6, size=sum(sizes)).astype(np.float64))
+    r = 13
+    w0 = rng.random((r, n)).astype(np.float32).astype(np.float64)
+    f0 = rng.random((r, len(sizes))).astype(np.float32).astype(np.float64)
+    plan = DevicePlan(V, r, "fp32", order="counter", order_seed=2024)
+    ids = rng.permutation(r)
+    plan.set_factors(w0, f0, order=ids)
+    mg, mo, tg, to, sg, so = _compare_half_step(plan, "F", ids, 0.01, 0.05, iteration=3)
+    _check(mg, mo, tg, to, "counter buckets")
+    _check_stats(sg, so)
+
+
+def test_counter_order_factorize(cuda_ok):
+    """factorize(order="counter"): deterministic, and the objective decreases
+    like the shared order's (a different but equally valid randomisation)."""
+    from paper_1604_04026_b200 import NmfConfig, RegConfig, factorize, synth
+
+    spec = _spec("C3").scaled(m=6000)
+    V = synth.generate(spec)
+    w0, f0 = synth.initial_factors(spec)
+    import paper_1604_04026_b200 as kb
+
+    res = {}
+    for order in ("counter", "counter", "shared"):
+        cfg = NmfConfig(rank=spec.rank, reg=spec.reg, max_outer_iters=8, rel_obj_tol=0.0, seed=spec.seed,
+                        precision="fp32", order=order)
+        out = factorize(V, cfg, kb.FactorPair(kb.DenseFactor(w0), kb.DenseFactor(f0)))
+        res.setdefault(order, []).append(out)
+    a, b = res["counter"]
+    assert np.array_equal(a.factors.w.values, b.factors.w.values)
+    assert np.array_equal(a.factors.f.values, b.factors.f.values)
+    tot_c = [rec.total_objective for rec in a.log.records]
+    tot_s = [rec.total_objective for rec in res["shared"][0].log.records]
+    print("counter", tot_c)
+    print("shared ", tot_s)
+    assert all(y <= x * (1 + 1e-6) for x, y in zip(tot_c, tot_c[1:]))
+    # a different randomisation moves the early trajectory a lot (SURVEY.md
+    # A.10: up to 31%); require comparable progress, not equal values
+    assert (tot_c[0] - tot_c[-1]) > 0.5 * (tot_s[0] - tot_s[-1])
+    assert not np.array_equal(a.factors.f.values, res["shared"][0].factors.f.values)
 
 
 def test_every_bucket_kernel(cuda_ok):
