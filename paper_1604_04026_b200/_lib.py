@@ -9,6 +9,7 @@ CUDA failure inside a call is raised as ``RuntimeError`` carrying
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -132,7 +133,7 @@ def load(path: Path | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("KLNMF_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"libklnmf.so not found at {p}: build it with `python -m paper_1604_04026_b200.build` "

@@ -642,7 +642,7 @@ namespace cg = cooperative_groups;
 constexpr int CL_NT = 256, CL_NR = 8, CL_NS = 4, CL_PER_SM = 2;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
 constexpr int CL_MAXG = 512;          // most CTAs in one cooperative row group
-constexpr size_t COOP_GROUP_BYTES = 128 + 2 * CL_MAXG * NV * sizeof(double);
+constexpr size_t COOP_GROUP_BYTES = 2 * CL_MAXG * NV * 2 * sizeof(unsigned long long) + 128;
 
 struct GroupRed {
     double wred[2][CL_NT / 32][NV];
@@ -759,53 +759,76 @@ struct ClusterReducer {
     }
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// Sum over the G CTAs of a cooperative row group through global memory.
+// Each partial travels as two 8-byte words {32 value bits, 32-bit round tag}
+// (the LL idea of NCCL's low-latency protocol): 8-byte accesses are
+// single-copy atomic, so a reader that sees the current tag in both words
+// has the whole value and per-location coherence rules out stale words --
+// no fence is needed anywhere.  Arrival is signalled by a relaxed atomic on
+// the group counter that one lane per CTA polls (one word of polling
+// traffic); should a counter increment overtake its data, the tag check
+// simply waits for the data.  Tags are round + 1 (memset 0 = empty) and never
+// repeat, so parity double-buffering is enough: a slot of round n is
+// rewritten at round n + 2, after every reader of round n has published
+// round n + 1.  Warp i then sums value i over the G CTAs (lane c reads CTA c)
+// in a fixed order.
+__device__ __forceinline__ ulonglong2 ld_relaxed_v2(const unsigned long long *p) {
+    ulonglong2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_relaxed_v2(unsigned long long *p, unsigned long long a, unsigned long long b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
 
-// Sum over the G CTAs of a cooperative row group through global memory: each
-// CTA publishes its partials, bumps the group's monotonic counter and waits
-// for the round's G arrivals.
 struct CoopReducer {
     GroupRed &R;
-    double *slots;      // [2][NV][CL_MAXG], double-buffered by round parity
-    unsigned *counter;  // arrivals, G per round
+    unsigned long long *slots;  // [2][NV][CL_MAXG][2] tagged words
+    unsigned *counter;          // arrivals, G per round
     int G, rank;
     unsigned round;
     __device__ __forceinline__ void operator()(double (&v)[NV], int buf) {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        cta_partial(v, R, buf);
+        const double s = cta_partial(v, R, buf);
         if (G == 1) {
-            if (w == 0 && lane < NV) R.tot[buf][lane] = R.cpart[buf][lane];
+            if (w == 0 && lane < NV) R.tot[buf][lane] = s;
             __syncthreads();
             return;
         }
-        // slot layout [round parity][value][CTA]: value i of all CTAs is contiguous
-        double *cur = slots + (size_t)(round & 1) * CL_MAXG * NV;
+        const unsigned b = round & 1u;
+        const unsigned long long tag = round + 1u;
+        if (w == 0 && lane < NV) {
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(s);
+            st_relaxed_v2(slots + (((size_t)b * NV + lane) * CL_MAXG + rank) * 2, (bits & 0xffffffff00000000ull) | tag,
+                          (bits << 32) | tag);
+        }
         if (w == 0) {
-            if (lane < NV) {
-                __stcg(cur + (size_t)lane * CL_MAXG + rank, R.cpart[buf][lane]);
-                __threadfence();
-            }
             __syncwarp();
-            const unsigned target = (unsigned)G * (round + 1);
             if (lane == 0) {
                 atomicAdd(counter, 1u);
-                while (ld_acquire(counter) < target) __nanosleep(32);
+                const unsigned target = (unsigned)G * (round + 1u);
+                while (*(volatile unsigned *)counter < target) __nanosleep(32);
             }
         }
         __syncthreads();
-        // lane 0 of warp 0 acquired the counter; the barrier orders these loads after it
-        if (w < NV) {  // warp i sums value i over the G CTAs, all loads in flight at once
-            const double *col = cur + (size_t)w * CL_MAXG;
-            double s = 0.0;
-#pragma unroll
-            for (int c0 = 0; c0 < CL_MAXG; c0 += 32)
-                if (c0 < G) s += (c0 + lane < G) ? __ldcg(col + c0 + lane) : 0.0;
-            s = warp_sum(s);
-            if (lane == 0) R.tot[buf][w] = s;
+        if (w < NV) {
+            const unsigned long long *col = slots + ((size_t)b * NV + w) * CL_MAXG * 2;
+            double acc = 0.0;
+            for (int c0 = 0; c0 < G; c0 += 32) {
+                const int c = c0 + lane;
+                double x = 0.0;
+                if (c < G) {
+                    ulonglong2 q = ld_relaxed_v2(col + 2 * c);
+                    while ((unsigned)q.x != (unsigned)tag || (unsigned)q.y != (unsigned)tag) {
+                        __nanosleep(32);
+                        q = ld_relaxed_v2(col + 2 * c);
+                    }
+                    x = __longlong_as_double((long long)((q.x & 0xffffffff00000000ull) | (q.y >> 32)));
+                }
+                acc += x;
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) R.tot[buf][w] = acc;
         }
         __syncthreads();
         ++round;
@@ -1042,7 +1065,8 @@ __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_cluster_kernel(const k
 }
 
 // schedule: [n_waves][gridDim.x] int4 (item slot or -1, rank, G, group id);
-// sync: per group, a 128-byte counter line then 2*CL_MAXG*NV doubles.
+// sync: per group, [2][NV][CL_MAXG] tagged 16-byte reduction slots, then a
+// 128-byte line holding the arrival counter (CoopReducer).
 // A row group's waits only point to rows of the same or an earlier wave and
 // every CTA is resident (cooperative launch), so the schedule cannot deadlock.
 
@@ -1056,7 +1080,8 @@ __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_coop_kernel(const klnm
         const int4 job = schedule[(size_t)wv * gridDim.x + blockIdx.x];
         if (job.x < 0) continue;
         unsigned char *gb = sync + (size_t)job.w * COOP_GROUP_BYTES;
-        CoopReducer red{R, reinterpret_cast<double *>(gb + 128), reinterpret_cast<unsigned *>(gb), job.z, job.y, 0u};
+        CoopReducer red{R, reinterpret_cast<unsigned long long *>(gb),
+                        reinterpret_cast<unsigned *>(gb + COOP_GROUP_BYTES - 128), job.z, job.y, 0u};
         __syncthreads();  // shared buffers of the previous row are no longer read
         solve_slice(a, job.x, job.y, job.z, red, R, smem_raw, ssum);
     }
@@ -1178,7 +1203,7 @@ extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *sche
     cudaStream_t st = as_stream(stream);
     const size_t smem = slice_smem(args->rp);
     KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, smem));
-    KLNMF_CHECK(cudaMemsetAsync(sync, 0, (size_t)n_groups * COOP_GROUP_BYTES, st));
+    KLNMF_CHECK(cudaMemsetAsync(sync, 0, (size_t)n_groups * COOP_GROUP_BYTES, st));  // tag 0: empty
     klnmf_solve_args_t a = *args;
     const int4 *sched = static_cast<const int4 *>(schedule);
     unsigned char *sy = static_cast<unsigned char *>(sync);

@@ -42,10 +42,12 @@ def main(rep, which, obj, func_sub, n=40):
     ti, ts = sum(ins.values()), sum(smp.values())
     src = Path(__file__).resolve().parents[1] / "paper_1604_04026_b200/csrc/solve_fast.cu"
     text = src.read_text().splitlines()
-    for ln in sorted(ins, key=lambda k: -ins[k])[:n]:
+    key = smp if "--samples" in sys.argv else ins
+    for ln in sorted(ins, key=lambda k: -key[k])[:n]:
         code = text[ln - 1].strip()[:70] if ln else "?"
         print(f"  line {ln}: inst {100 * ins[ln] / ti:5.1f}%  samples {100 * smp[ln] / ts:5.1f}%  {code}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4], int(sys.argv[5]) if len(sys.argv) > 5 else 40)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(args[0], int(args[1]), args[2], args[3], int(args[4]) if len(args) > 4 else 40)
