@@ -314,10 +314,13 @@ void oracle_row_sums(const double *factor, int64_t r, int64_t n, double *out) {
  * coordinate visited tt-th), arithmetic is fp64, the maintained product t of
  * every stored entry is carried between half-steps, and each Newton step
  * rounds the coordinate to fp32 so t stays consistent with the stored factor.
- * The gradient is the reference's _grad_hess (_kernels.py:24-36) rewritten
- * with per-entry u = v/(t+eps), z = u/(t+eps): g = sum_a + alpha*x + beta -
- * sum(u*a), h = alpha + sum(z*a*a).  The control flow is solve_column's
- * (_kernels.py:73-118) verbatim.                                            */
+ * Per entry the state is u = v/(t+eps) and vi = 1/v: the reference's
+ * _grad_hess (_kernels.py:24-36) becomes g = sum_a + alpha*x + beta -
+ * sum(u*a), h = alpha + sum(z*a*a) with z = u*u*vi, a move t' = t + delta*a
+ * becomes u' = u/q with q = 1 + delta*a*u*vi (clamp t' < 0 -> 0 as
+ * _kernels.py:105-106: q < eps*u*vi -> u' = v/eps), and t = 1/(u*vi) - eps
+ * is written back at the end.  eps_div > 0.  The control flow is
+ * solve_column's (_kernels.py:73-118) verbatim.                             */
 /* fp32 storage value of a non-negative coordinate; subnormals are flushed to
  * zero (the device kernels widen stored values with integer arithmetic that
  * is exact for zero and normal floats only). */
@@ -395,15 +398,15 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
         if (s > cap_s) cap_s = s;
     }
     double *u = (double *)malloc(sizeof(double) * (size_t)(cap_s + 1));
-    double *z = (double *)malloc(sizeof(double) * (size_t)(cap_s + 1));
+    double *vi = (double *)malloc(sizeof(double) * (size_t)(cap_s + 1));
     for (int64_t q = 0; q < n_items; ++q) {
         int64_t j = items ? items[q] : q;
         int64_t lo = ptr[j], s = ptr[j + 1] - lo;
         double *tj = t + lo;
         for (int64_t p = 0; p < s; ++p) {
-            double rinv = 1.0 / (tj[p] + eps_div);
-            u[p] = (double)val[lo + p] * rinv;
-            z[p] = u[p] * rinv;
+            const double v = (double)val[lo + p];
+            u[p] = v * (1.0 / (tj[p] + eps_div));
+            vi[p] = 1.0 / v;
         }
         stats[STAT_PASSES] += 1;
         /* shared order: storage order; counter order: chunks in the
@@ -420,8 +423,9 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
         for (int64_t p = 0; p < s; ++p) {                                 \
             double a = (double)fixed[(int64_t)idx[lo + p] * rp + tt];     \
             if (a != 0.0) {                                               \
-                gp += u[p] * a;                                           \
-                hp += (z[p] * a) * a;                                     \
+                double z = (u[p] * u[p]) * vi[p];                         \
+                gp = fma(u[p], a, gp);                                    \
+                hp = fma(z * a, a, hp);                                   \
             }                                                             \
         }                                                                 \
         g = sum_fixed[tt] + alpha * x + beta - gp;                        \
@@ -457,12 +461,11 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
                     for (int64_t p = 0; p < s; ++p) {
                         double a = (double)fixed[(int64_t)idx[lo + p] * rp + tt];
                         if (a != 0.0) {
-                            double tn = tj[p] + delta * a;
-                            if (tn < 0.0) tn = 0.0;
-                            tj[p] = tn;
-                            double rinv = 1.0 / (tn + eps_div);
-                            u[p] = (double)val[lo + p] * rinv;
-                            z[p] = u[p] * rinv;
+                            /* the device's operation sequence (fused q, u times 1/q) */
+                            double pp = u[p] * vi[p]; /* 1/(t+eps) */
+                            double q = fma(pp, delta * a, 1.0);
+                            if (q < eps_div * pp) u[p] = 1.0 / (vi[p] * eps_div); /* t' clamped to 0 */
+                            else u[p] = u[p] * (1.0 / q);
                         }
                     }
                 }
@@ -472,7 +475,11 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
 #undef EVAL
             moving[j * rp + tt] = (float)x;
         }
+        for (int64_t p = 0; p < s; ++p) {
+            double tn = 1.0 / (u[p] * vi[p]) - eps_div;
+            tj[p] = tn < 0.0 ? 0.0 : tn;
+        }
     }
     free(u);
-    free(z);
+    free(vi);
 }

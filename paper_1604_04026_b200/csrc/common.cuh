@@ -69,7 +69,9 @@ __host__ __device__ inline void chunk_order(uint64_t seed, uint32_t iter, uint32
             w[3] = side;
             philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
         }
-        const uint32_t j = (uint32_t)(((uint64_t)w[k & 3] * (uint32_t)(i + 1)) >> 32);
+        const int wk = k & 3;  // register selects, no local-memory array
+        const uint32_t word = wk == 0 ? w[0] : (wk == 1 ? w[1] : (wk == 2 ? w[2] : w[3]));
+        const uint32_t j = (uint32_t)(((uint64_t)word * (uint32_t)(i + 1)) >> 32);
         const uint8_t tmp = order[i];
         order[i] = order[j];
         order[j] = tmp;

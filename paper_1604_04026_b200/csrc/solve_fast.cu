@@ -6,10 +6,12 @@
 //   * the maintained product t is kept on the column support S only and is
 //     CARRIED between half-steps (t at entry (i,j) is <W_i, F_j> for both
 //     sides), so no subproblem recomputes it from the fixed factor;
-//   * per entry the kernel keeps u = v/(t+eps) and z = u/(t+eps) so that
+//   * per entry the kernel keeps only u = v/(t+eps) and vi = 1/v (16 bytes):
 //     _grad_hess (_kernels.py:24-36) becomes g = sum_a + alpha*x + beta -
-//     sum(u*a), h = alpha + sum(z*a*a); entries with a == 0 are skipped as in
-//     the reference;
+//     sum(u*a), h = alpha + sum(z*a*a) with z = u/(t+eps) = u*u*vi, and a move
+//     t' = t + delta*a (clamped at 0, _kernels.py:105-106) becomes
+//     u' = u / (1 + delta*a*u*vi); t = 1/(u*vi) - eps is written back once at
+//     the end.  The compact state is what sets how many entries stay on chip;
 //   * every Newton step rounds the coordinate to fp32 (the storage type), so
 //     t stays consistent with the stored factors;
 //   * coordinates are visited in storage order (factors are stored in the
@@ -25,6 +27,7 @@
 //     components and reduced sums are read from shared memory by index, so
 //     the Newton/update code exists once per kernel and stays in the
 //     instruction cache.
+// eps_div > 0 is required (u is finite); the exact mode covers eps_div = 0.
 //
 // Kernels (one launch per nnz bucket, largest subproblems first):
 //   solve_warp_kernel<L, NPL>    L <= 32 lanes per subproblem, 32/L
@@ -65,25 +68,25 @@ __device__ __forceinline__ bool enters(double g, double x, double eg) {
     return (g < -eg) || (fabs(g) > eg && x > eg);  // _kernels.py:78
 }
 
-// fp32 -> fp64 of a stored factor value on the integer pipes (the F2F
-// conversion runs on the quarter-rate XU pipe).  Exact for the values the
-// fp32-mode factors can hold: non-negative and finite (DenseFactor
-// validation, sparse.py:184) and zero or normal -- subnormals are flushed to
-// zero at every store (round_store, klnmf_layout_to_device).
-__device__ __forceinline__ double widen(float f) {
-#ifdef KLNMF_WIDEN_INT
-    const unsigned b = __float_as_uint(f);
-    const unsigned hi = (b >> 3) + (b ? 0x38000000u : 0u);  // exponent rebias 127 -> 1023
-    return __hiloint2double((int)hi, (int)(b << 29));
-#else
-    return (double)f;
-#endif
-}
+// fp32 -> fp64 of a stored factor value (non-negative and finite, DenseFactor
+// validation sparse.py:184; subnormals are flushed to zero at every store).
+__device__ __forceinline__ double widen(float f) { return (double)f; }
 
 // Rounds a non-negative coordinate to its fp32 storage value (subnormals to 0).
 __device__ __forceinline__ double round_store(double x) {
     const float f = __double2float_rn(x);
     return f < 1.17549435e-38f ? 0.0 : (double)f;
+}
+
+// 1/x: MUFU approximation refined twice (full fp64 accuracy up to the last
+// bit or so); x > 0 (eps_div > 0 keeps every t + eps positive).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
 }
 
 // One Newton step of the inner loop (_kernels.py:78-115), x rounded to fp32.
@@ -105,7 +108,7 @@ __device__ __forceinline__ double newton_step(double g, double h, double &x, int
         active = false;
         return delta;
     }
-    double target = x - g / h;
+    double target = x - g / h;  // IEEE division: once per step, and it keeps x's rounding exact
     if (target < 0.0) target = 0.0;
     const double xn = round_store(target);
     delta = xn - x;
@@ -124,88 +127,64 @@ __device__ __forceinline__ double newton_step(double g, double h, double &x, int
     return delta;
 }
 
-// 1/x: MUFU approximation refined by one Newton step (relative error ~1e-14,
-// far below the fp32 storage rounding of this mode).  ZCHK: x == 0 (only
-// possible with eps_div == 0) returns inf like the IEEE division.
-template <bool ZCHK = true>
-__device__ __forceinline__ double fast_rcp(double x) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    const double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    if (!ZCHK) return r;
-    return x == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : r;
+// Per-entry state (see the header): u = v/(t+eps), vi = 1/v.  Absent
+// (padding) entries hold u = vi = 0 and contribute exactly 0.
+__device__ __forceinline__ void entry_init(double t, float v, double eps, double &u, double &vi) {
+    const double vd = (double)v;
+    u = vd * fast_rcp(t + eps);
+    vi = v > 0.f ? fast_rcp(vd) : 0.0;
+}
+// z = u/(t+eps), the curvature weight of the entry
+__device__ __forceinline__ double entry_z(double u, double vi) { return (u * u) * vi; }
+// the maintained product written back at the end of the half-step
+__device__ __forceinline__ double entry_t(double u, double vi, double eps) {
+    return fmax(1.0 / (u * vi) - eps, 0.0);
+}
+// Move of the visited coordinate by delta: t' + eps = (t + eps) * q with
+// q = 1 + delta*a/(t+eps), so u' = u / q; the reference clamps t' at 0
+// (_kernels.py:105-106): t' < 0 <=> q < eps/(t+eps), and then u' = v/eps.
+// CLAMP = false when delta >= 0 (q >= 1: the clamp cannot fire).  Applied
+// branch-free to every entry: a == 0 gives q = 1 and leaves u unchanged.
+template <bool CLAMP>
+__device__ __forceinline__ void entry_update(double delta, double a, double eps, double &u, double vi) {
+    const double p = u * vi;                  // 1/(t+eps)
+    const double q = fma(p, delta * a, 1.0);  // (t'+eps)/(t+eps)
+    double un = u * fast_rcp(q);
+    if (CLAMP && q < eps * p) un = fast_rcp(vi * eps);
+    u = un;
 }
 
-// Maintained product of an entry and its u = v/(t+eps), z = u/(t+eps).
-template <bool ZCHK = true>
-__device__ __forceinline__ void entry_init(double tq, float v, double eps, double &t, double &u, double &z) {
-    t = tq;
-    const double ri = fast_rcp<ZCHK>(tq + eps);
-    u = (double)v * ri;
-    z = u * ri;
-}
-
-// Move of the visited coordinate by delta; the clamp at 0 is the reference's
-// (_kernels.py:105-106).  Applied branch-free to every entry: at a == 0 it
-// reproduces t, u and z bit for bit (fma(delta, 0, t) == t and u, z are
-// recomputed from the same t by the same formula), so the reference's
-// a != 0 test is implicit.
-__device__ __forceinline__ void entry_update(double delta, double av, float v, double eps, double &t, double &u,
-                                             double &z) {
-    entry_init(fmax(fma(delta, av, t), 0.0), v, eps, t, u, z);
-}
-
-// Specialised update: CLAMP = false when delta >= 0 (t, a >= 0 keep the sum
-// non-negative, so the clamp cannot fire), ZCHK = false when eps_div > 0.
-template <bool CLAMP, bool ZCHK>
-__device__ __forceinline__ void entry_update_m(double delta, double av, float v, double eps, double &t, double &u,
-                                               double &z) {
-    const double tn = fma(delta, av, t);
-    entry_init<ZCHK>(CLAMP ? fmax(tn, 0.0) : tn, v, eps, t, u, z);
-}
-
-// Calls f(CLAMP, ZCHK) as compile-time constants for a group-uniform move.
+// Calls f(CLAMP) as a compile-time constant for a group-uniform move.
 template <typename F>
-__device__ __forceinline__ void with_update_mode(bool any_negative, double eps, F &&f) {
-    if (eps > 0.0) {
-        if (any_negative) f(std::true_type{}, std::false_type{});
-        else f(std::false_type{}, std::false_type{});
-    } else {
-        f(std::true_type{}, std::true_type{});
-    }
+__device__ __forceinline__ void with_clamp(bool any_negative, F &&f) {
+    if (any_negative) f(std::true_type{});
+    else f(std::false_type{});
 }
 
 // Adds one entry's contribution to a coordinate's (g, h) partial sums.  The
-// reference skips a == 0 (_kernels.py:32).  With eps_div > 0, u and z are
-// finite, so an a == 0 term adds exactly +0.0 and the guard is dropped; GUARD
-// keeps it for eps_div == 0, where u may be inf.
-template <bool GUARD>
+// reference skips a == 0 (_kernels.py:32); u and z are finite (eps_div > 0),
+// so an a == 0 term adds exactly +0.0 and needs no test.
 __device__ __forceinline__ void accum(double &g, double &h, double u, double z, double av) {
-    if (!GUARD || av != 0.0) {
-        g = fma(u, av, g);
-        h = fma(z * av, av, h);
-    }
+    g = fma(u, av, g);
+    h = fma(z * av, av, h);
 }
 
-// Partials of the chunk's coordinates cc..C-1 from one entry's 16-byte chunk
-// (runtime cc; the eps_div == 0 path).
-template <bool GUARD>
-__device__ __forceinline__ void accum_chunk(double (&red)[NV], const float4 &a4, double u, double z, int cc) {
-    if (cc <= 0) accum<GUARD>(red[0], red[C + 0], u, z, widen(a4.x));
-    if (cc <= 1) accum<GUARD>(red[1], red[C + 1], u, z, widen(a4.y));
-    if (cc <= 2) accum<GUARD>(red[2], red[C + 2], u, z, widen(a4.z));
-    accum<GUARD>(red[3], red[C + 3], u, z, widen(a4.w));
-}
-
-// Same with a compile-time first coordinate: no predication, no conversions
-// of the chunk components that are already consumed.
+// Partials of the chunk's coordinates CC..C-1 from one entry's 16-byte chunk
+// (compile-time first coordinate: no predication, no conversions of the
+// components already consumed).
 template <int CC>
 __device__ __forceinline__ void accum_from(double (&red)[NV], const float4 &a4, double u, double z) {
-    if (CC <= 0) accum<false>(red[0], red[C + 0], u, z, widen(a4.x));
-    if (CC <= 1) accum<false>(red[1], red[C + 1], u, z, widen(a4.y));
-    if (CC <= 2) accum<false>(red[2], red[C + 2], u, z, widen(a4.z));
-    accum<false>(red[3], red[C + 3], u, z, widen(a4.w));
+    if (CC <= 0) accum(red[0], red[C + 0], u, z, widen(a4.x));
+    if (CC <= 1) accum(red[1], red[C + 1], u, z, widen(a4.y));
+    if (CC <= 2) accum(red[2], red[C + 2], u, z, widen(a4.z));
+    accum(red[3], red[C + 3], u, z, widen(a4.w));
+}
+// runtime first coordinate (the rare spilled entries of the long-row kernels)
+__device__ __forceinline__ void accum_chunk(double (&red)[NV], const float4 &a4, double u, double z, int cc) {
+    if (cc <= 0) accum(red[0], red[C + 0], u, z, widen(a4.x));
+    if (cc <= 1) accum(red[1], red[C + 1], u, z, widen(a4.y));
+    if (cc <= 2) accum(red[2], red[C + 2], u, z, widen(a4.z));
+    accum(red[3], red[C + 3], u, z, widen(a4.w));
 }
 
 // Calls f(std::integral_constant<int, cc>) for a runtime cc in [0, C).
@@ -335,21 +314,18 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     if (counter && gl == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
     __syncwarp();
 
-    double t[NPL], u[NPL], z[NPL];
-    float v[NPL];
-    const float *row[NPL];  // gather source of each entry (row 0 for absent entries)
+    double u[NPL], vi[NPL];
+    int roff[NPL];  // gather source of each entry (row 0 for absent entries)
 #pragma unroll
     for (int e = 0; e < NPL; ++e) {
         const int p = gl + e * L;
         if (p < s) {
             const int64_t q = lo + p;
-            row[e] = fixed + (int64_t)a.side.idx[q] * rp;
-            v[e] = val[q];
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[q] : q], v[e], pm.eps_div, t[e], u[e], z[e]);
+            roff[e] = a.side.idx[q] * rp;
+            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[q] : q], val[q], pm.eps_div, u[e], vi[e]);
         } else {
-            row[e] = fixed;
-            v[e] = 0.f;
-            t[e] = u[e] = z[e] = 0.0;  // contributes exactly 0 to every sum
+            roff[e] = 0;
+            u[e] = vi[e] = 0.0;  // contributes exactly 0 to every sum
         }
     }
     const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * tid;
@@ -359,7 +335,8 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
             const unsigned base = ring_s + 16u * NT * NPL * (chunk % STAGES);
             const int pc = phys(chunk);
 #pragma unroll
-            for (int e = 0; e < NPL; ++e) cp_async16(base + 16u * NT * e, row[e] + pc * C, gl + e * L < s);
+            for (int e = 0; e < NPL; ++e)
+                cp_async16(base + 16u * NT * e, fixed + roff[e] + pc * C, gl + e * L < s);
         }
         cp_commit();
     };
@@ -383,15 +360,11 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                if (pm.eps_div > 0.0) {
-                    with_cc(cc, [&](auto ccv) {
+                with_cc(cc, [&](auto ccv) {
 #pragma unroll
-                        for (int e = 0; e < NPL; ++e) accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], z[e]);
-                    });
-                } else {
-#pragma unroll
-                    for (int e = 0; e < NPL; ++e) accum_chunk<true>(red, Ach[e * NT], u[e], z[e], cc);
-                }
+                    for (int e = 0; e < NPL; ++e)
+                        accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], entry_z(u[e], vi[e]));
+                });
                 TReduce<L>::run(red, gl);
                 TReduce<L>::store(red, gl, tot);
                 __syncwarp();
@@ -410,25 +383,19 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 if (active) delta = newton_step(g, h, x, inner, active, again, pm, cnt);
                 if (__any_sync(FULL_MASK, delta != 0.0)) {
                     if (delta != 0.0) moved = true;
-                    // delta == 0 (groups not moving) leaves every entry bit-identical
-                    with_update_mode(__any_sync(FULL_MASK, delta < 0.0), pm.eps_div, [&](auto cl, auto zc) {
+                    // delta == 0 (groups not moving) leaves every entry unchanged (q = 1)
+                    with_clamp(__any_sync(FULL_MASK, delta < 0.0), [&](auto cl) {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            entry_update_m<decltype(cl)::value, decltype(zc)::value>(
-                                delta, widen(comp(Ach + e * NT, cc)), v[e], pm.eps_div, t[e], u[e], z[e]);
+                            entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, cc)), pm.eps_div, u[e],
+                                                              vi[e]);
                     });
                 }
                 if (__any_sync(FULL_MASK, again)) {
                     double g2 = 0.0, h2 = 0.0;
-                    if (pm.eps_div > 0.0) {
 #pragma unroll
-                        for (int e = 0; e < NPL; ++e)
-                            accum<false>(g2, h2, u[e], z[e], widen(comp(Ach + e * NT, cc)));
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < NPL; ++e)
-                            accum<true>(g2, h2, u[e], z[e], widen(comp(Ach + e * NT, cc)));
-                    }
+                    for (int e = 0; e < NPL; ++e)
+                        accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, cc)));
 #pragma unroll
                     for (int o = L / 2; o > 0; o >>= 1) {
                         g2 += __shfl_xor_sync(FULL_MASK, g2, o);
@@ -451,7 +418,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
         for (int k = gl; k < r; k += L) moving[j * rp + a.perm_out[k]] = xo[k];
 #pragma unroll
         for (int e = 0; e < NPL; ++e)
-            if (gl + e * L < s) a.t_out[lo + gl + e * L] = t[e];
+            if (gl + e * L < s) a.t_out[lo + gl + e * L] = entry_t(u[e], vi[e], pm.eps_div);
     }
     flush_stats(cnt, gl == 0 && valid, a.stats, true);
 }
@@ -468,6 +435,17 @@ struct BlockSums {
         const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
         TReduce<32>::run(v, lane);
         if ((lane & 3) == 0) w[buf][wi][lane >> 2] = v[0];
+        __syncthreads();
+    }
+    // (g, h) of one coordinate into slots 0, 1: one halving level, then a
+    // butterfly on the kept value (lanes < 16 end with g, the others with h)
+    __device__ __forceinline__ void reduce2(double g, double h, int buf) {
+        const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+        const bool up = (lane & 16) != 0;
+        double keep = (up ? h : g) + __shfl_xor_sync(FULL_MASK, up ? g : h, 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(FULL_MASK, keep, o);
+        if ((lane & 15) == 0) w[buf][wi][lane >> 4] = keep;
         __syncthreads();
     }
     __device__ __forceinline__ double get(int buf, int i) const {
@@ -504,21 +482,18 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     for (int k = tid; k < r; k += NT) ssum[k] = a.sum_pos[k];
     for (int k = tid; k < r; k += NT) xs[k] = moving[j * rp + a.perm_in[k]];
 
-    double t[NPL], u[NPL], z[NPL];
-    float v[NPL];
-    const float *row[NPL];
+    double u[NPL], vi[NPL];
+    int roff[NPL];
 #pragma unroll
     for (int e = 0; e < NPL; ++e) {
         const int p = tid + e * NT;
         if (p < s) {
             const int64_t q = lo + p;
-            row[e] = fixed + (int64_t)a.side.idx[q] * rp;
-            v[e] = val[q];
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[q] : q], v[e], pm.eps_div, t[e], u[e], z[e]);
+            roff[e] = a.side.idx[q] * rp;
+            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[q] : q], val[q], pm.eps_div, u[e], vi[e]);
         } else {
-            row[e] = fixed;
-            v[e] = 0.f;
-            t[e] = u[e] = z[e] = 0.0;
+            roff[e] = 0;
+            u[e] = vi[e] = 0.0;
         }
     }
     const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * tid;
@@ -534,7 +509,8 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
             const unsigned base = ring_s + 16u * NT * NPL * (chunk % STAGES);
             const int pc = phys(chunk);
 #pragma unroll
-            for (int e = 0; e < NPL; ++e) cp_async16(base + 16u * NT * e, row[e] + pc * C, tid + e * NT < s);
+            for (int e = 0; e < NPL; ++e)
+                cp_async16(base + 16u * NT * e, fixed + roff[e] + pc * C, tid + e * NT < s);
         }
         cp_commit();
     };
@@ -558,15 +534,11 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                if (pm.eps_div > 0.0) {
-                    with_cc(cc, [&](auto ccv) {
+                with_cc(cc, [&](auto ccv) {
 #pragma unroll
-                        for (int e = 0; e < NPL; ++e) accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], z[e]);
-                    });
-                } else {
-#pragma unroll
-                    for (int e = 0; e < NPL; ++e) accum_chunk<true>(red, Ach[e * NT], u[e], z[e], cc);
-                }
+                    for (int e = 0; e < NPL; ++e)
+                        accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], entry_z(u[e], vi[e]));
+                });
                 bs.reduce(red, buf);
                 cur = buf;
                 buf ^= 1;
@@ -584,27 +556,19 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                 const double delta = newton_step(g, h, x, inner, active, again, pm, cnt);
                 if (delta != 0.0) {
                     moved = true;
-                    with_update_mode(delta < 0.0, pm.eps_div, [&](auto cl, auto zc) {
+                    with_clamp(delta < 0.0, [&](auto cl) {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            entry_update_m<decltype(cl)::value, decltype(zc)::value>(
-                                delta, widen(comp(Ach + e * NT, cc)), v[e], pm.eps_div, t[e], u[e], z[e]);
+                            entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, cc)), pm.eps_div, u[e],
+                                                              vi[e]);
                     });
                 }
                 if (again) {
-                    double ev[NV];
+                    double g2 = 0.0, h2 = 0.0;
 #pragma unroll
-                    for (int i = 0; i < NV; ++i) ev[i] = 0.0;
-                    if (pm.eps_div > 0.0) {
-#pragma unroll
-                        for (int e = 0; e < NPL; ++e)
-                            accum<false>(ev[0], ev[1], u[e], z[e], widen(comp(Ach + e * NT, cc)));
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < NPL; ++e)
-                            accum<true>(ev[0], ev[1], u[e], z[e], widen(comp(Ach + e * NT, cc)));
-                    }
-                    bs.reduce(ev, buf);
+                    for (int e = 0; e < NPL; ++e)
+                        accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, cc)));
+                    bs.reduce2(g2, h2, buf);
                     g = (base + pm.alpha * x) - bs.get(buf, 0);
                     h = pm.alpha + bs.get(buf, 1);
                     buf ^= 1;
@@ -621,7 +585,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     for (int k = tid; k < r; k += NT) moving[j * rp + a.perm_out[k]] = xo[k];
 #pragma unroll
     for (int e = 0; e < NPL; ++e)
-        if (tid + e * NT < s) a.t_out[lo + tid + e * NT] = t[e];
+        if (tid + e * NT < s) a.t_out[lo + tid + e * NT] = entry_t(u[e], vi[e], pm.eps_div);
     flush_stats(cnt, tid == 0, a.stats, false);
 }
 
@@ -636,10 +600,11 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 // moves of the chunk read it from there.
 namespace cg = cooperative_groups;
 
-// 256 threads and at most ~113 KB of shared memory per CTA: two slices (of
-// different rows, or of one row) share an SM, so one CTA's reduction and
-// gather latency overlaps the other's arithmetic.
-constexpr int CL_NT = 256, CL_NR = 8, CL_NS = 4, CL_PER_SM = 2;
+// 256 threads and ~101 KB of shared memory per CTA: two slices (of different
+// rows, or of one row) share an SM, so one CTA's reduction and gather latency
+// overlaps the other's arithmetic.  16 resident entries per thread: 8 in
+// registers (u, 1/v, row offset), 8 in shared memory.
+constexpr int CL_NT = 256, CL_NR = 8, CL_NS = 8, CL_PER_SM = 2;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
 constexpr int CL_MAXG = 512;          // most CTAs in one cooperative row group
 constexpr size_t COOP_GROUP_BYTES = 2 * CL_MAXG * NV * 2 * sizeof(unsigned long long) + 128;
@@ -841,11 +806,9 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                                             GroupRed &R, unsigned char *smem_raw, const double *ssum) {
     constexpr int NT = CL_NT, NR = CL_NR, NS = CL_NS;
     float4 *cache = reinterpret_cast<float4 *>(smem_raw);             // [NR+NS][NT]: current chunk
-    double *Ts = reinterpret_cast<double *>(cache + (NR + NS) * NT);  // [NS][NT]
-    double *Us = Ts + NS * NT;
-    double *Zs = Us + NS * NT;
-    int2 *VO = reinterpret_cast<int2 *>(Zs + NS * NT);    // (float bits of v, row offset)
-    float *xs = reinterpret_cast<float *>(VO + NS * NT);  // [2][rps]: input row, result
+    double *Us = reinterpret_cast<double *>(cache + (NR + NS) * NT);  // [NS][NT]
+    double *VIs = Us + NS * NT;                                       // [NS][NT]
+    float *xs = reinterpret_cast<float *>(VIs + NS * NT);             // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
     uint8_t *cord = reinterpret_cast<uint8_t *>(xo + (a.rp | 1));  // counter order
 
@@ -863,14 +826,12 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const int64_t cn = min(s, c0 + per) - c0;  // entries of this CTA
     const int64_t base = lo + c0;              // global entry index of local entry 0
     const double eps = pm.eps_div;
-    double *Tg = a.t_out + base;  // spilled entries: t in t_out, u/z in scratch
-    double *Ug = a.scratch + base;
-    double *Zg = a.scratch + a.side.nnz + base;
+    double *Ug = a.scratch + base;  // spilled entries: u and vi in scratch
+    double *VIg = a.scratch + a.side.nnz + base;
 
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
-    double t[NR], u[NR], z[NR];
-    float v[NR];
+    double u[NR], vi[NR];
     int off[NR];
 #pragma unroll
     for (int e = 0; e < NR; ++e) {
@@ -878,12 +839,10 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         if (i < cn) {
             const int64_t g = base + i;
             off[e] = a.side.idx[g] * rp;
-            v[e] = val[g];
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], v[e], eps, t[e], u[e], z[e]);
+            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, u[e], vi[e]);
         } else {
             off[e] = -1;
-            v[e] = 0.f;
-            t[e] = u[e] = z[e] = 0.0;
+            u[e] = vi[e] = 0.0;
         }
     }
     int offs[NS];
@@ -893,20 +852,17 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         const int si = e * NT + tid;
         if (i < cn) {
             const int64_t g = base + i;
-            const float vv = val[g];
             offs[e] = a.side.idx[g] * rp;
-            VO[si] = make_int2(__float_as_int(vv), offs[e]);
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], vv, eps, Ts[si], Us[si], Zs[si]);
+            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, Us[si], VIs[si]);
         } else {
             offs[e] = -1;
-            VO[si] = make_int2(0, -1);
-            Ts[si] = Us[si] = Zs[si] = 0.0;
+            Us[si] = VIs[si] = 0.0;
         }
     }
     const int64_t spill0 = (int64_t)(NR + NS) * NT;  // first spilled local entry
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const int64_t g = base + i;
-        entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, Tg[i], Ug[i], Zg[i]);
+        entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, Ug[i], VIg[i]);
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
@@ -937,28 +893,19 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                if (eps > 0.0) {
-                    with_cc(cc, [&](auto ccv) {
-                        constexpr int CC = decltype(ccv)::value;
+                with_cc(cc, [&](auto ccv) {
+                    constexpr int CC = decltype(ccv)::value;
 #pragma unroll
-                        for (int e = 0; e < NR; ++e) accum_from<CC>(red, A[e * NT], u[e], z[e]);
+                    for (int e = 0; e < NR; ++e) accum_from<CC>(red, A[e * NT], u[e], entry_z(u[e], vi[e]));
 #pragma unroll
-                        for (int e = 0; e < NS; ++e)
-                            accum_from<CC>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid]);
-                    });
-                    for (int64_t i = spill0 + tid; i < cn; i += NT)
-                        accum_chunk<false>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), Ug[i],
-                                           Zg[i], cc);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < NR; ++e) accum_chunk<true>(red, A[e * NT], u[e], z[e], cc);
-#pragma unroll
-                    for (int e = 0; e < NS; ++e)
-                        accum_chunk<true>(red, A[(NR + e) * NT], Us[e * NT + tid], Zs[e * NT + tid], cc);
-                    for (int64_t i = spill0 + tid; i < cn; i += NT)
-                        accum_chunk<true>(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), Ug[i],
-                                          Zg[i], cc);
-                }
+                    for (int e = 0; e < NS; ++e) {
+                        const double uu = Us[e * NT + tid];
+                        accum_from<CC>(red, A[(NR + e) * NT], uu, entry_z(uu, VIs[e * NT + tid]));
+                    }
+                });
+                for (int64_t i = spill0 + tid; i < cn; i += NT)
+                    accum_chunk(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), Ug[i],
+                                entry_z(Ug[i], VIg[i]), cc);
                 reduce(red, buf);
                 cur = buf;
                 buf ^= 1;
@@ -974,49 +921,45 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             while (active) {  // uniform over the group
                 bool again = false;
                 const double delta = newton_step(g, h, x, inner, active, again, pm, cnt);
-                double ev[NV];
+                const bool upd = delta != 0.0;  // uniform over the group
+                if (upd) moved = true;
+                double g2 = 0.0, h2 = 0.0;
+                // apply the move and, if the loop continues, re-evaluate this coordinate
+                if (upd || again) {
+                    with_clamp(delta < 0.0, [&](auto cl) {
+                        constexpr bool CL = decltype(cl)::value;
 #pragma unroll
-                for (int i = 0; i < NV; ++i) ev[i] = 0.0;
-                // apply the move (and, if the loop continues, re-evaluate this coordinate)
-                if (delta != 0.0 || again) {
-                    const bool upd = delta != 0.0;  // uniform over the group
-                    if (upd) moved = true;
+                        for (int e = 0; e < NR; ++e) {  // register entries: branch-free
+                            const double av = widen(comp(A + e * NT, cc));
+                            if (upd) entry_update<CL>(delta, av, eps, u[e], vi[e]);
+                            if (again) accum(g2, h2, u[e], entry_z(u[e], vi[e]), av);
+                        }
 #pragma unroll
-                    for (int e = 0; e < NR; ++e) {  // register entries: branch-free
-                        const double av = widen(comp(A + e * NT, cc));
-                        if (upd) entry_update(delta, av, v[e], eps, t[e], u[e], z[e]);
-                        if (eps > 0.0 || av != 0.0) accum<false>(ev[0], ev[1], u[e], z[e], av);
-                    }
-#pragma unroll
-                    for (int e = 0; e < NS; ++e) {
-                        const int si = e * NT + tid;
-                        const double av = widen(comp(A + (NR + e) * NT, cc));
-                        if (av != 0.0) {
-                            double tn = Ts[si], uu = Us[si], zz = Zs[si];
-                            if (delta != 0.0) {
-                                entry_update(delta, av, __int_as_float(VO[si].x), eps, tn, uu, zz);
-                                Ts[si] = tn;
+                        for (int e = 0; e < NS; ++e) {
+                            const int si = e * NT + tid;
+                            const double av = widen(comp(A + (NR + e) * NT, cc));
+                            double uu = Us[si];
+                            const double vv = VIs[si];
+                            if (upd) {
+                                entry_update<CL>(delta, av, eps, uu, vv);
                                 Us[si] = uu;
-                                Zs[si] = zz;
                             }
-                            accum<false>(ev[0], ev[1], uu, zz, av);
+                            if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
-                    }
-                    for (int64_t i = spill0 + tid; i < cn; i += NT) {
-                        const double av = (double)__ldg(fixed + (int64_t)a.side.idx[base + i] * rp + tt);
-                        if (av != 0.0) {
-                            double tn = Tg[i], uu = Ug[i], zz = Zg[i];
-                            if (delta != 0.0) {
-                                entry_update(delta, av, val[base + i], eps, tn, uu, zz);
-                                Tg[i] = tn;
+                        for (int64_t i = spill0 + tid; i < cn; i += NT) {
+                            const double av = (double)__ldg(fixed + (int64_t)a.side.idx[base + i] * rp + tt);
+                            double uu = Ug[i];
+                            const double vv = VIg[i];
+                            if (upd) {
+                                entry_update<CL>(delta, av, eps, uu, vv);
                                 Ug[i] = uu;
-                                Zg[i] = zz;
                             }
-                            accum<false>(ev[0], ev[1], uu, zz, av);
+                            if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
-                    }
+                    });
                 }
                 if (again) {
+                    double ev[NV] = {g2, h2};
                     reduce(ev, buf);
                     g = (sb + pm.alpha * x) - R.tot[buf][0];
                     h = pm.alpha + R.tot[buf][1];
@@ -1034,10 +977,12 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         for (int kk = tid; kk < r; kk += NT) moving[j * rp + a.perm_out[kk]] = xo[kk];
 #pragma unroll
     for (int e = 0; e < NR; ++e)
-        if (off[e] >= 0) a.t_out[base + tid + (int64_t)e * NT] = t[e];
+        if (off[e] >= 0) a.t_out[base + tid + (int64_t)e * NT] = entry_t(u[e], vi[e], eps);
 #pragma unroll
     for (int e = 0; e < NS; ++e)
-        if (offs[e] >= 0) a.t_out[base + tid + (int64_t)(NR + e) * NT] = Ts[e * NT + tid];
+        if (offs[e] >= 0)
+            a.t_out[base + tid + (int64_t)(NR + e) * NT] = entry_t(Us[e * NT + tid], VIs[e * NT + tid], eps);
+    for (int64_t i = spill0 + tid; i < cn; i += NT) a.t_out[base + i] = entry_t(Ug[i], VIg[i], eps);
     flush_stats(cnt, cq == 0 && tid == 0, a.stats, false);
 }
 
@@ -1116,7 +1061,7 @@ const FastKernel kFast[] = {
 constexpr int kNumFast = sizeof(kFast) / sizeof(kFast[0]);
 
 inline size_t slice_smem(int rp) {
-    return (size_t)CL_NE * CL_NT * sizeof(float4) + (size_t)CL_NS * CL_NT * (3 * sizeof(double) + sizeof(int2)) +
+    return (size_t)CL_NE * CL_NT * sizeof(float4) + (size_t)CL_NS * CL_NT * 2 * sizeof(double) +
            2 * sizeof(float) * (size_t)(rp | 1) + MAX_CHUNKS + 16;
 }
 
@@ -1142,6 +1087,7 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (args->rp > KMAX_RP) return set_error_msg(1, "klnmf_solve_fast: rank above 256 is not supported in fp32 mode");
     if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
         return set_error_msg(1, "klnmf_solve_fast: bad coordinate order mode");
+    if (!(args->eps_div > 0.0)) return set_error_msg(1, "klnmf_solve_fast: the fp32 mode needs eps_div > 0");
     const FastKernel &k = kFast[kernel_id];
     if (k.cluster < 0) return set_error_msg(1, "klnmf_solve_fast: the long-row bucket runs through klnmf_solve_coop");
     if (k.cluster > 0) {
@@ -1200,6 +1146,7 @@ extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *sche
     if (args->scratch == nullptr) return set_error_msg(1, "klnmf_solve_coop: needs a scratch buffer");
     if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
         return set_error_msg(1, "klnmf_solve_coop: bad coordinate order mode");
+    if (!(args->eps_div > 0.0)) return set_error_msg(1, "klnmf_solve_coop: the fp32 mode needs eps_div > 0");
     cudaStream_t st = as_stream(stream);
     const size_t smem = slice_smem(args->rp);
     KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, smem));

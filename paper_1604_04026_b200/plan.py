@@ -352,6 +352,9 @@ class DevicePlan:
         """
         if self.order_mode == _lib.ORDER_COUNTER and iteration is None:
             raise ValueError("the counter coordinate order needs the iteration number")
+        if self.fp32 and not tol.eps_div > 0.0:
+            raise ValueError("the fp32 mode needs eps_div > 0 (its per-entry state is v/(t+eps_div)); "
+                             "use precision='fp64' for eps_div = 0")
         ids = np.asarray(ids, dtype=np.int64)
         fixed_name = "W" if which == "F" else "F"
         if self.order[fixed_name] is None or not np.array_equal(self.order[fixed_name], ids):
