@@ -48,7 +48,10 @@ namespace {
 
 constexpr int C = 4;          // coordinates per chunk (16 B of fp32 per entry)
 constexpr int NV = 2 * C;     // reduced values per pass: g partials then h partials
-constexpr int STAGES = 3;     // cp.async ring depth of the warp/block kernels
+// cp.async ring depth of the warp/block kernels: 3 stages; 2 when a thread
+// holds many entries (the ring is the shared-memory budget that sets how many
+// subproblems are resident per SM)
+constexpr int ring_stages(int npl) { return npl >= 10 ? 2 : 3; }
 constexpr int KMAX_RP = 256;  // largest padded rank of the fp32 kernels (row sums staged in smem)
 
 struct Counters {
@@ -276,6 +279,7 @@ template <int L, int NPL>
 __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_t a) {
     constexpr int NT = 128;
     constexpr int GPB = NT / L;  // groups per block
+    constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);                 // [STAGES][NPL][NT]
     float *xs_all = reinterpret_cast<float *>(ring + STAGES * NPL * NT);  // [GPB][2][rps]
@@ -459,6 +463,7 @@ struct BlockSums {
 // One subproblem per block, NPL register entries per thread.
 template <int NT, int NPL>
 __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_t a) {
+    constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);             // [STAGES][NPL][NT]
     float *xs = reinterpret_cast<float *>(ring + STAGES * NPL * NT);  // [2][rps]: input row, result
@@ -1049,8 +1054,8 @@ struct FastKernel {
 // W side's subproblem sizes concentrate (SURVEY.md §8(d) size profiles).
 const FastKernel kFast[] = {
     WK(1, 4),   WK(2, 4),   WK(4, 4),   WK(8, 4),   WK(8, 6),   WK(8, 8),   WK(16, 6),  WK(16, 8),
-    WK(32, 5),  WK(32, 6),  WK(32, 7),  WK(32, 8),  BK(64, 5),  BK(64, 6),  BK(64, 7),  BK(64, 8),
-    BK(128, 5), BK(128, 6), BK(128, 7), BK(128, 8), BK(256, 6), BK(256, 8), BK(512, 6), BK(512, 8),
+    WK(32, 5),  WK(32, 6),  WK(32, 7),  WK(32, 8),  WK(32, 10), WK(32, 12), WK(32, 14), WK(32, 16),
+    BK(64, 10), BK(64, 12), BK(64, 14), BK(64, 16), BK(128, 12), BK(128, 16), BK(256, 12), BK(256, 16),
     CK(2),      CK(4),      CK(8),      CK(16),
     // unbounded: the cooperative long-row kernel (klnmf_solve_coop, schedule built by the caller)
     {CL_NT, CL_NE, CL_NT, -1, nullptr, 1, 0, -1},
@@ -1117,7 +1122,7 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
         return 0;
     }
     const int64_t blocks = (args->n_items + k.gpb - 1) / k.gpb;
-    const size_t ring = sizeof(float4) * (size_t)STAGES * (size_t)k.ring_entries * (size_t)k.nt;
+    const size_t ring = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt;
     const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) +
                         (args->order_mode != KLNMF_ORDER_SHARED ? (size_t)k.gpb * MAX_CHUNKS : 0) + 16;
     if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
