@@ -146,6 +146,9 @@ int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream);
 /* fp32-storage / fp64-arithmetic solver.  kernel_id selects the bucket kernel:
  * lanes-per-subproblem L and entries-per-lane NPL (klnmf_fast_kernel_info). */
 int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, void *stream);
+/* Sets the launch attributes of every fp32 kernel for padded rank rp once
+ * (call before capturing launches into a CUDA graph). */
+int klnmf_prepare_fast(int32_t rp);
 int klnmf_fast_kernel_count(void);
 /* capacity (max nnz per subproblem) and lanes of kernel_id; capacity < 0 = unbounded */
 int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t *lanes, int32_t *npl);
@@ -207,10 +210,25 @@ int klnmf_kl_data_term_dev(const klnmf_side_t *csc, const void *w, const void *f
                            const int32_t *wpos, const int32_t *fpos, int32_t r, int fp32,
                            double eps_div, double *out_host, void *stream);
 
+/* fp32 mode: the KL data term from the maintained products t (fp64, one per
+ * entry, in the order of val): sum v*log(v/(t+eps)) - v, a streaming pass
+ * instead of nnz r-dots.  Deterministic.  Result (fp64) in *out_host. */
+int klnmf_kl_data_term_t(const float *val, const double *t, int64_t nnz, double eps_div, double *out_host,
+                         void *stream);
+
 /* factor statistics over the r real columns: out_host[0] = sum x^2, [1] = sum x,
  * [2] = number of exact zeros (as double).  Deterministic. */
 int klnmf_factor_stats(const void *fac, int64_t n_items, int32_t rp, int32_t r, int fp32,
                        double *out_host, void *stream);
+
+/* Host <-> device bulk transfers through reusable pinned staging buffers,
+ * converting on host threads (the API's int64 / fp64 arrays vs the device's
+ * int32 / fp32).  Synchronous with respect to the host; n elements. */
+int klnmf_upload_i64_as_i32(const int64_t *src_host, int64_t n, int32_t *dst_dev, void *stream);
+int klnmf_upload_f64_as_f32(const double *src_host, int64_t n, float *dst_dev, void *stream);
+int klnmf_upload_f64(const double *src_host, int64_t n, double *dst_dev, void *stream);
+int klnmf_download_f32_as_f64(const float *src_dev, int64_t n, double *dst_host, void *stream);
+int klnmf_download_f64(const double *src_dev, int64_t n, double *dst_host, void *stream);
 
 #ifdef __cplusplus
 }

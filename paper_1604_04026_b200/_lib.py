@@ -32,6 +32,7 @@ EXPORTS = (
     "klnmf_row_sums",
     "klnmf_solve_exact",
     "klnmf_solve_fast",
+    "klnmf_prepare_fast",
     "klnmf_fast_kernel_count",
     "klnmf_fast_kernel_info",
     "klnmf_coop_info",
@@ -45,7 +46,13 @@ EXPORTS = (
     "klnmf_bucketize",
     "klnmf_init_t",
     "klnmf_kl_data_term_dev",
+    "klnmf_kl_data_term_t",
     "klnmf_factor_stats",
+    "klnmf_upload_i64_as_i32",
+    "klnmf_upload_f64_as_f32",
+    "klnmf_upload_f64",
+    "klnmf_download_f32_as_f64",
+    "klnmf_download_f64",
 )
 
 STATS_LEN = 4
@@ -109,6 +116,7 @@ _SIGS = {
     "klnmf_row_sums": ([P, I64, I64, P], INT),
     "klnmf_solve_exact": ([ctypes.POINTER(SolveArgs), P], INT),
     "klnmf_solve_fast": ([ctypes.POINTER(SolveArgs), INT, P], INT),
+    "klnmf_prepare_fast": ([I32], INT),
     "klnmf_fast_kernel_count": ([], INT),
     "klnmf_fast_kernel_info": ([INT, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)], INT),
     "klnmf_coop_info": ([I32, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I64)], INT),
@@ -122,7 +130,13 @@ _SIGS = {
     "klnmf_bucketize": ([P, I64, I64, P, INT, P, P, P], INT),
     "klnmf_init_t": ([ctypes.POINTER(Side), P, P, I32, P, P, I32, P, P], INT),
     "klnmf_kl_data_term_dev": ([ctypes.POINTER(Side), P, P, I32, P, P, I32, INT, D, P, P], INT),
+    "klnmf_kl_data_term_t": ([P, P, I64, D, P, P], INT),
     "klnmf_factor_stats": ([P, I64, I32, I32, INT, P, P], INT),
+    "klnmf_upload_i64_as_i32": ([P, I64, P, P], INT),
+    "klnmf_upload_f64_as_f32": ([P, I64, P, P], INT),
+    "klnmf_upload_f64": ([P, I64, P, P], INT),
+    "klnmf_download_f32_as_f64": ([P, I64, P, P], INT),
+    "klnmf_download_f64": ([P, I64, P, P], INT),
 }
 
 _lib = None

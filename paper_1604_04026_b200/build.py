@@ -24,7 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I", str(INCLUDE)]
 # exact mode mirrors the reference's FMA-free numba codegen (SURVEY.md finding 3)
 PER_FILE = {"solve_exact.cu": ["-fmad=false"]}
-SOURCES = ["abi_host.cu", "solve_exact.cu", "solve_fast.cu", "factor_ops.cu", "sparse_build.cu"]
+SOURCES = ["abi_host.cu", "solve_exact.cu", "solve_fast.cu", "factor_ops.cu", "sparse_build.cu", "host_io.cu"]
 
 
 def nvcc() -> str:
@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-pthread", "-o", str(LIB), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -32,7 +32,7 @@ cudaError_t ensure_smem(const void *fn, size_t bytes) {
         const void *fn;
         size_t bytes;
     };
-    static Entry cache[64];
+    static Entry cache[256];
     static int n = 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -45,7 +45,7 @@ cudaError_t ensure_smem(const void *fn, size_t bytes) {
             return e;
         }
     const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess && n < 64) cache[n++] = Entry{key, bytes};
+    if (e == cudaSuccess && n < 256) cache[n++] = Entry{key, bytes};
     return e;
 }
 

@@ -198,6 +198,45 @@ extern "C" int klnmf_factor_stats(const void *fac, int64_t n_items, int32_t rp, 
     return 0;
 }
 
+// KL data term from the maintained products (fp32 mode): fixed grid, each
+// block sums a fixed contiguous range in a fixed tree, then one warp sums the
+// block partials in order -- deterministic for a given nnz.
+constexpr int KL_BLOCKS = 1184, KL_NT = 256;  // 8 x 148 SMs
+__global__ void kl_t_partial(const float *val, const double *t, int64_t nnz, double eps, double *partial) {
+    __shared__ double sh[KL_NT / 32];
+    const int64_t per = (nnz + KL_BLOCKS - 1) / KL_BLOCKS;
+    const int64_t lo = (int64_t)blockIdx.x * per, hi = min(nnz, lo + per);
+    double s = 0.0;
+    for (int64_t q = lo + threadIdx.x; q < hi; q += KL_NT) {
+        const double v = (double)val[q];
+        s += v * log(v / (t[q] + eps)) - v;  // _kernels.py:158
+    }
+    const double b = block_sum_det<KL_NT>(s, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = b;
+}
+__global__ void kl_t_final(const double *partial, double *out) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < KL_BLOCKS; b += 32) s += partial[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if (threadIdx.x == 0) *out = s;
+}
+
+extern "C" int klnmf_kl_data_term_t(const float *val, const double *t, int64_t nnz, double eps_div,
+                                    double *out_host, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    double *partial = nullptr;
+    KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (KL_BLOCKS + 1), st));
+    kl_t_partial<<<KL_BLOCKS, KL_NT, 0, st>>>(val, t, nnz, eps_div, partial);
+    KLNMF_CHECK_LAUNCH("kl_t_partial");
+    kl_t_final<<<1, 32, 0, st>>>(partial, partial + KL_BLOCKS);
+    KLNMF_CHECK_LAUNCH("kl_t_final");
+    KLNMF_CHECK(cudaMemcpyAsync(out_host, partial + KL_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(cudaFreeAsync(partial, st));
+    KLNMF_CHECK(cudaStreamSynchronize(st));
+    return 0;
+}
+
 extern "C" int klnmf_init_t(const klnmf_side_t *side, const float *fixed, const float *moving, int32_t rp,
                             const int32_t *fixed_pos, const int32_t *moving_pos, int32_t r, double *t,
                             void *stream) {

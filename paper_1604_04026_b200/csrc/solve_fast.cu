@@ -1085,6 +1085,37 @@ extern "C" int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t 
     return 0;
 }
 
+static bool g_nonportable_set = false;
+
+// Sets every fp32 kernel's launch attributes (dynamic shared memory for the
+// larger, counter-order layout; non-portable cluster sizes) for padded rank
+// rp, so that later launches -- in particular inside CUDA-graph capture --
+// issue no attribute calls.
+extern "C" int klnmf_prepare_fast(int32_t rp) {
+    if (rp % 4 != 0 || rp > KMAX_RP) return set_error_msg(1, "klnmf_prepare_fast: bad padded rank");
+    cudaFuncAttributes fa;
+    KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)solve_coop_kernel));  // loads the module now
+    for (int id = 0; id < kNumFast; ++id) {
+        const FastKernel &k = kFast[id];
+        if (k.fn) KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)k.fn));
+        if (k.cluster < 0) {
+            KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, slice_smem(rp)));
+        } else if (k.cluster > 0) {
+            KLNMF_CHECK(ensure_smem((const void *)k.fn, slice_smem(rp)));
+            if (k.cluster > 8 && !g_nonportable_set) {
+                KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                g_nonportable_set = true;
+            }
+        } else {
+            const size_t smem = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries *
+                                    (size_t)k.nt +
+                                2 * sizeof(float) * (size_t)k.gpb * (size_t)(rp | 1) + (size_t)k.gpb * MAX_CHUNKS + 16;
+            if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
+        }
+    }
+    return 0;
+}
+
 extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, void *stream) {
     if (kernel_id < 0 || kernel_id >= kNumFast) return set_error_msg(1, "klnmf_solve_fast: bad kernel id");
     if (args->n_items <= 0) return 0;
@@ -1100,11 +1131,9 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
             return set_error_msg(1, "klnmf_solve_fast: the cluster kernel needs a scratch buffer");
         const size_t smem = slice_smem(args->rp);
         KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
-        if (k.cluster > 8) {
-            static bool nonportable = false;
-            if (!nonportable)
-                KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            nonportable = true;
+        if (k.cluster > 8 && !g_nonportable_set) {
+            KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            g_nonportable_set = true;
         }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(args->n_items * k.cluster), 1, 1);

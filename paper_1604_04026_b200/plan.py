@@ -31,10 +31,14 @@ and NCCL collectives.  All arithmetic runs in libklnmf.so.
 from __future__ import annotations
 
 import ctypes
+import os
+import time
 import dataclasses
 
 import numpy as np
 import torch
+
+_TIMING = bool(os.environ.get("KLNMF_TIMING"))
 
 from . import _lib
 from .subproblem import SolveStats, Tolerances
@@ -126,8 +130,13 @@ class DevicePlan:
             self.stream_ptr = torch.cuda.current_stream(dev).cuda_stream
             # CSC of V (F-side) uploaded once; CSC of V^T (W-side) built on device
             csc_ptr = torch.from_numpy(V.col_ptr).to(dev)
-            csc_idx = torch.from_numpy(V.row_idx).to(dev).to(torch.int32)
-            csc_val = torch.from_numpy(V.values).to(dev).to(self.vdt)
+            csc_idx = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            csc_val = torch.empty(max(self.nnz, 1), dtype=self.vdt, device=dev)
+            row_idx = np.ascontiguousarray(V.row_idx, dtype=np.int64)
+            values = np.ascontiguousarray(V.values, dtype=np.float64)
+            _lib.call("klnmf_upload_i64_as_i32", row_idx.ctypes.data, self.nnz, csc_idx.data_ptr(), self.stream_ptr)
+            _lib.call("klnmf_upload_f64_as_f32" if self.fp32 else "klnmf_upload_f64", values.ctypes.data,
+                      self.nnz, csc_val.data_ptr(), self.stream_ptr)
             csr_ptr = torch.empty(self.n + 1, dtype=torch.int64, device=dev)
             csr_idx = torch.empty(self.nnz, dtype=torch.int32, device=dev)
             csr_val = torch.empty(self.nnz, dtype=self.vdt, device=dev)
@@ -183,6 +192,8 @@ class DevicePlan:
             self._perm_event = None
             self.use_graphs = True
             self._capturing = False
+            if self.fp32:
+                _lib.call("klnmf_prepare_fast", self.rp)
             self._graphs = {}
             self._warm = set()
             self._pos = torch.zeros(2, self.rp, dtype=torch.int32, device=dev)
@@ -288,7 +299,9 @@ class DevicePlan:
             o = torch.from_numpy(self._padded(self.order[name])).to(self.dev)
             _lib.call("klnmf_layout_from_device", self.factors[name].data_ptr(), self.r, n_items, o.data_ptr(),
                       self.rp, int(self.fp32), dst.data_ptr(), self.stream_ptr)
-            out.append(dst.cpu().numpy())
+            host = np.empty((self.r, n_items), dtype=np.float64)
+            _lib.call("klnmf_download_f64", dst.data_ptr(), host.size, host.ctypes.data, self.stream_ptr)
+            out.append(host)
         return out[0], out[1]
 
     # ------------------------------------------------------------------
@@ -411,12 +424,14 @@ class DevicePlan:
         self._perm_event.record(torch.cuda.current_stream(self.dev))
 
     def _capture(self, key):
-        """Capture one side's launch sequence (after one eager warm-up run of
-        it, so the library's one-time function attributes are already set)."""
+        """Capture one side's launch sequence into a CUDA graph.  The fp32
+        kernels' one-time launch attributes were set at plan construction
+        (klnmf_prepare_fast); the exact mode warms up eagerly once first."""
         which, alpha, beta, tol, dev_sums, with_events = key
-        if key not in self._warm:
+        if not self.fp32 and key not in self._warm:
             self._warm.add(key)
             return None  # run eagerly this time
+        t_start = time.perf_counter() if _TIMING else 0.0
         graph = torch.cuda.CUDAGraph()
         capture_stream = torch.cuda.Stream(self.dev)
         evs: list = []
@@ -433,6 +448,9 @@ class DevicePlan:
             self.stream_ptr = saved
             self._capturing = False
         self._graphs[key] = (graph, evs)
+        if _TIMING:
+            print(f"[klnmf] captured {which} half-step graph in {1e3 * (time.perf_counter() - t_start):.1f} ms",
+                  flush=True)
         return self._graphs[key]
 
     def _launch(self, which, alpha, beta, tol, dev_sums, events) -> None:
@@ -526,16 +544,23 @@ class DevicePlan:
 
     def objective(self, alpha1=0.0, alpha2=0.0, beta1=0.0, beta2=0.0, eps_div=1e-16):
         """(kl, total, sparsity_w, sparsity_f) -- full_objective, solver.py:219-234."""
-        side = self.sides["F"]
-        s = side.side_struct()
-        wpos = self._padded(np.argsort(self.order["W"]))
-        fpos = self._padded(np.argsort(self.order["F"]))
-        self._h2d_i32(self._pos[0], wpos)
-        self._h2d_i32(self._pos[1], fpos)
         data = ctypes.c_double()
-        _lib.call("klnmf_kl_data_term_dev", ctypes.byref(s), self.factors["W"].data_ptr(),
-                  self.factors["F"].data_ptr(), self.rp, self._pos[0].data_ptr(), self._pos[1].data_ptr(),
-                  self.r, int(self.fp32), float(eps_div), ctypes.byref(data), self.stream_ptr)
+        if self.fp32 and self.t_current is not None:
+            # fp32 mode carries t = <W_i, F_j> for every entry (all ranks hold all
+            # of it after the exchange): one streaming pass over (v, t)
+            side = self.sides["F"] if self.t_current == "csc" else self.sides["W"]
+            _lib.call("klnmf_kl_data_term_t", side.val.data_ptr(), self.t[self.t_current].data_ptr(),
+                      self.nnz, float(eps_div), ctypes.byref(data), self.stream_ptr)
+        else:
+            side = self.sides["F"]
+            s = side.side_struct()
+            wpos = self._padded(np.argsort(self.order["W"]))
+            fpos = self._padded(np.argsort(self.order["F"]))
+            self._h2d_i32(self._pos[0], wpos)
+            self._h2d_i32(self._pos[1], fpos)
+            _lib.call("klnmf_kl_data_term_dev", ctypes.byref(s), self.factors["W"].data_ptr(),
+                      self.factors["F"].data_ptr(), self.rp, self._pos[0].data_ptr(), self._pos[1].data_ptr(),
+                      self.r, int(self.fp32), float(eps_div), ctypes.byref(data), self.stream_ptr)
         kl = float(data.value) + float(self.row_sums_natural("W") @ self.row_sums_natural("F"))
         st = {}
         for name in ("W", "F"):
