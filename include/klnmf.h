@@ -230,6 +230,15 @@ int klnmf_upload_f64(const double *src_host, int64_t n, double *dst_dev, void *s
 int klnmf_download_f32_as_f64(const float *src_dev, int64_t n, double *dst_host, void *stream);
 int klnmf_download_f64(const double *src_dev, int64_t n, double *dst_host, void *stream);
 
+/* MatrixMarket coordinate files (native reader, the reference's rules and
+ * messages, sparse.py:217-268).  klnmf_mm_header reports the size line;
+ * klnmf_mm_read fills 0-based int64 rows/cols and fp64 values (nnz_cap >=
+ * nnz).  Malformed files return KLNMF_MM_FORMAT_ERROR with the reference's
+ * message in klnmf_last_error(). */
+#define KLNMF_MM_FORMAT_ERROR 2
+int klnmf_mm_header(const char *path, int64_t *n_rows, int64_t *n_cols, int64_t *nnz);
+int klnmf_mm_read(const char *path, int64_t nnz_cap, int64_t *rows, int64_t *cols, double *vals);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,9 +53,12 @@ EXPORTS = (
     "klnmf_upload_f64",
     "klnmf_download_f32_as_f64",
     "klnmf_download_f64",
+    "klnmf_mm_header",
+    "klnmf_mm_read",
 )
 
 STATS_LEN = 4
+MM_FORMAT_ERROR = 2
 ORDER_SHARED, ORDER_COUNTER = 0, 1
 STAT_CAP_HITS, STAT_DEGENERATE, STAT_INNER_ITERS, STAT_PASSES = range(4)
 
@@ -137,6 +140,8 @@ _SIGS = {
     "klnmf_upload_f64": ([P, I64, P, P], INT),
     "klnmf_download_f32_as_f64": ([P, I64, P, P], INT),
     "klnmf_download_f64": ([P, I64, P, P], INT),
+    "klnmf_mm_header": ([ctypes.c_char_p, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)], INT),
+    "klnmf_mm_read": ([ctypes.c_char_p, I64, P, P, P], INT),
 }
 
 _lib = None
