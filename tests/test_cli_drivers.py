@@ -1,0 +1,77 @@
+"""Drivers and command line: the reference's
+bench/cli surface on the GPU backend, device counts in place of threads."""
+import csv
+import json
+
+import numpy as np
+import pytest
+
+from paper_1604_04026_b200 import ConvergenceLog, IterationRecord
+from paper_1604_04026_b200 import cli, drivers
+
+
+def test_usage_errors_exit_1(capsys):
+    assert cli.main([]) == 1
+    assert cli.main(["run", "--out", "x"]) == 1  # neither --input nor --config
+    assert cli.main(["scaling", "--config", "C1", "--input", "a.mtx", "--out", "x"]) == 1
+    assert cli.main(["run", "--config", "C1", "--out", "x", "--precision", "fp16"]) == 1
+
+
+def test_scaling_grid_validation(tmp_path):
+    with pytest.raises(ValueError):
+        drivers.scaling_report("C1", [], [1], 1, tmp_path, available_devices=1)
+    with pytest.raises(ValueError, match="requested"):
+        drivers.scaling_report("C1", [10], [1, 2], 1, tmp_path, available_devices=1)
+    with pytest.raises(ValueError):
+        drivers.scaling_report("C1", [10], [0], 1, tmp_path, available_devices=1)
+
+
+def test_runtime_error_exit_2(tmp_path, capsys):
+    assert cli.main(["run", "--input", str(tmp_path / "missing.mtx"), "--out", str(tmp_path / "o")]) == 2
+    assert "error" in capsys.readouterr().err
+
+
+def test_log_csv_round_trip(tmp_path):
+    log = ConvergenceLog()
+    for i in range(1, 4):
+        log.append(IterationRecord(i, 0.1 * i, 10.0 / i, 11.0 / i, 0.25, 0.5))
+    drivers.write_log_csv(log, tmp_path / "log.csv")
+    back = drivers.read_log_csv(tmp_path / "log.csv")
+    assert back.records == log.records
+
+
+def test_load_dataset_names(tmp_path):
+    v = drivers.load_dataset("C1@m=200")
+    assert v.shape == (2000, 200)
+    with pytest.raises(ValueError):
+        drivers.load_dataset("C1@q=3")
+    from paper_1604_04026_b200 import save_matrix_market
+
+    save_matrix_market(v, tmp_path / "v.mtx")
+    w = drivers.load_dataset(str(tmp_path / "v.mtx"))
+    assert np.array_equal(w.row_idx, v.row_idx)
+
+
+@pytest.mark.gpu
+def test_cli_run_writes_reference_outputs(cuda_ok, tmp_path):
+    out = tmp_path / "run"
+    rc = cli.main(["run", "--config", "C1@m=300", "--rank", "5", "--max-iters", "3", "--tol", "0",
+                   "--precision", "fp32", "--out", str(out)])
+    assert rc == 0
+    for f in ("log.csv", "W.mtx", "W.tsv", "F.mtx", "F.tsv", "summary.json"):
+        assert (out / f).exists(), f
+    s = json.loads((out / "summary.json").read_text())
+    log = drivers.read_log_csv(out / "log.csv")
+    assert s["iterations"] == len(log) >= 1
+    assert abs(s["final_total_objective"] - log.records[-1].total_objective) <= 1e-6 * abs(s["final_total_objective"])
+
+
+@pytest.mark.gpu
+def test_cli_scaling_one_device(cuda_ok, tmp_path):
+    rc = cli.main(["scaling", "--config", "C1@m=300", "--r-values", "4,8", "--device-values", "1", "--iters", "2",
+                   "--precision", "fp32", "--out", str(tmp_path)])
+    assert rc == 0
+    rows = list(csv.reader(open(tmp_path / "scaling.csv")))
+    assert rows[0] == ["r", "n_devices", "wall_seconds"]
+    assert [(int(a), int(b)) for a, b, _ in rows[1:]] == [(4, 1), (8, 1)]
+    assert all(float(c) > 0 for _, _, c in rows[1:])
