@@ -80,6 +80,28 @@ int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx, const doub
 /* _kernels.kl_data_term(col_ptr, row_idx, values, w, f, eps_div) (_kernels.py:148):
  * sum over stored entries of v*log(v/((W^T F)_ij + eps)) - v.  w is (r, n_rows),
  * f is (r, n_cols).  Result in *out. */
+/* sweep_range with solve_column's max_passes (_kernels.py:53-120): the
+ * passes over a column repeat until one moves nothing (the stationarity
+ * certificate of subproblem.solve_column) or max_passes is reached. */
+int klnmf_sweep_range_passes(const int64_t *col_ptr, const int64_t *row_idx, const double *values, const double *at,
+                             const double *sum_a, double *moving, int64_t j_lo, int64_t j_hi, const int64_t *ids,
+                             double alpha, double beta, double eps_grad, double eps_x, double eps_div,
+                             int64_t inner_cap, int64_t max_passes, int64_t r, int64_t n_fix, int64_t n_mov,
+                             int64_t *stats);
+
+/* replaces _kernels.kkt_violation (_kernels.py:176-190) for every column of
+ * x (r, n_mov): out (r, n_mov) in the reference layout, bit-identical. */
+int klnmf_kkt_violation(const int64_t *col_ptr, const int64_t *row_idx, const double *values, const double *at,
+                        const double *sum_a, const double *x, double alpha, double beta, double eps_grad,
+                        double eps_x, double eps_div, int64_t r, int64_t n_fix, int64_t n_mov, double *out);
+
+/* replaces _kernels.mu_update_range (_kernels.py:193-214): moving[:, j] for
+ * j in [j_lo, j_hi) rescaled in place, bit-identical (num_buf is device
+ * scratch). */
+int klnmf_mu_update_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values, const double *fixed,
+                          double *moving, const double *sum_fixed, double eps_mu, int64_t j_lo, int64_t j_hi,
+                          int64_t r, int64_t n_fix, int64_t n_mov);
+
 int klnmf_kl_data_term(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
                        const double *w, const double *f, double eps_div, int64_t r,
                        int64_t n_rows, int64_t n_cols, double *out);
@@ -135,6 +157,11 @@ typedef struct {
     uint32_t order_side;
     uint64_t order_seed;
     const uint32_t *order_iter;
+    /* exact mode: passes over the coordinates per subproblem, repeated until
+     * one moves nothing (solve_column's max_passes, _kernels.py:70-120);
+     * 0 or 1 = the single pass of sweep_range */
+    int32_t max_passes;
+    int32_t reserved0;
 } klnmf_solve_args_t;
 
 #define KLNMF_ORDER_SHARED 0
@@ -142,6 +169,14 @@ typedef struct {
 
 /* exact fp64 solver (bit-identical to _kernels.sweep_range, one warp per subproblem) */
 int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream);
+/* exact KKT violations (_kernels.kkt_violation) of every listed subproblem at
+ * its current x; out (n_mov, rp) by position, device */
+int klnmf_kkt_exact(const klnmf_solve_args_t *args, double *out, void *stream);
+/* exact multiplicative update (_kernels.mu_update_range) of the listed
+ * subproblems; factors (n, rp) item-major in natural order, ratio_scratch nnz */
+int klnmf_mu_update_dev(const klnmf_side_t *side, const double *fixed, double *moving, const double *sum_fixed,
+                        int32_t r, int32_t rp, double eps_mu, const int32_t *items, int64_t n_items,
+                        double *ratio_scratch, void *stream);
 
 /* fp32-storage / fp64-arithmetic solver.  kernel_id selects the bucket kernel:
  * lanes-per-subproblem L and entries-per-lane NPL (klnmf_fast_kernel_info). */

@@ -324,6 +324,61 @@ void oracle_row_sums(const double *factor, int64_t r, int64_t n, double *out) {
 /* fp32 storage value of a non-negative coordinate; subnormals are flushed to
  * zero (the device kernels widen stored values with integer arithmetic that
  * is exact for zero and normal floats only). */
+/* kkt_violation, _kernels.py:176-190, for every column of x (r, n_mov):
+ * out (r, n_mov).  compute_ax on the support (bitwise equal to the dense
+ * product there, SURVEY.md finding 2). */
+void oracle_kkt_violation(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                          const double *at, int64_t r, int64_t n_fix, const double *sum_a,
+                          const double *x, int64_t n_mov, double alpha, double beta, double eps_grad,
+                          double eps_x, double eps_div, double *out) {
+    int64_t cap = 1;
+    for (int64_t j = 0; j < n_mov; ++j)
+        if (col_ptr[j + 1] - col_ptr[j] > cap) cap = col_ptr[j + 1] - col_ptr[j];
+    double *t = (double *)malloc(sizeof(double) * (size_t)cap);
+    double *xj = (double *)malloc(sizeof(double) * (size_t)r);
+    for (int64_t j = 0; j < n_mov; ++j) {
+        const int64_t lo = col_ptr[j], s = col_ptr[j + 1] - lo;
+        for (int64_t k = 0; k < r; ++k) xj[k] = x[k * n_mov + j];
+        compute_ax_support(at, r, n_fix, xj, row_idx + lo, s, t);
+        for (int64_t k = 0; k < r; ++k) {
+            double g, h;
+            grad_hess(k, row_idx + lo, values + lo, s, at, n_fix, t, 1, sum_a, xj[k], alpha, beta, eps_div, &g,
+                      &h);
+            double v;
+            if (xj[k] <= eps_grad) {
+                v = -g - eps_grad;
+            } else {
+                double scale = eps_x * xj[k] * h;
+                if (!(scale > eps_grad)) scale = eps_grad; /* max(eps_grad, scale) */
+                v = fabs(g) - scale;
+            }
+            out[k * n_mov + j] = v > 0.0 ? v : 0.0; /* max(0.0, v) */
+        }
+    }
+    free(t);
+    free(xj);
+}
+
+/* mu_update_range, _kernels.py:193-214 (moving rescaled in place). */
+void oracle_mu_update_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                            const double *fixed, double *moving, const double *sum_fixed, double eps_mu,
+                            int64_t j_lo, int64_t j_hi, int64_t r, int64_t n_fix, int64_t n_mov) {
+    double *num = (double *)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+    for (int64_t j = j_lo; j < j_hi; ++j) {
+        for (int64_t k = 0; k < r; ++k) num[k] = 0.0;
+        for (int64_t p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+            const int64_t i = row_idx[p];
+            double d = 0.0;
+            for (int64_t k = 0; k < r; ++k) d += fixed[k * n_fix + i] * moving[k * n_mov + j];
+            const double ratio = values[p] / (d + eps_mu);
+            for (int64_t k = 0; k < r; ++k) num[k] += fixed[k * n_fix + i] * ratio;
+        }
+        for (int64_t k = 0; k < r; ++k)
+            moving[k * n_mov + j] = moving[k * n_mov + j] * (num[k] + eps_mu) / (sum_fixed[k] + eps_mu);
+    }
+    free(num);
+}
+
 /* ------------------------------------------------------------------ */
 /* Counter-based coordinate order (north-star (c)).  Not part
  * of the reference: it replaces the reference's single ids permutation per

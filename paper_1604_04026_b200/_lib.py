@@ -28,9 +28,14 @@ EXPORTS = (
     "klnmf_event_record",
     "klnmf_chunk_order",
     "klnmf_sweep_range",
+    "klnmf_sweep_range_passes",
+    "klnmf_kkt_violation",
+    "klnmf_mu_update_range",
     "klnmf_kl_data_term",
     "klnmf_row_sums",
     "klnmf_solve_exact",
+    "klnmf_kkt_exact",
+    "klnmf_mu_update_dev",
     "klnmf_solve_fast",
     "klnmf_prepare_fast",
     "klnmf_fast_kernel_count",
@@ -106,6 +111,8 @@ class SolveArgs(ctypes.Structure):
         ("order_side", ctypes.c_uint32),
         ("order_seed", ctypes.c_uint64),
         ("order_iter", P),
+        ("max_passes", I32),
+        ("reserved0", I32),
     ]
 
 
@@ -115,9 +122,14 @@ _SIGS = {
     "klnmf_event_record": ([P, P, INT], INT),
     "klnmf_chunk_order": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, I32, P], INT),
     "klnmf_sweep_range": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, P], INT),
+    "klnmf_sweep_range_passes": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, I64, P], INT),
+    "klnmf_kkt_violation": ([P, P, P, P, P, P, D, D, D, D, D, I64, I64, I64, P], INT),
+    "klnmf_mu_update_range": ([P, P, P, P, P, P, D, I64, I64, I64, I64, I64], INT),
     "klnmf_kl_data_term": ([P, P, P, P, P, D, I64, I64, I64, P], INT),
     "klnmf_row_sums": ([P, I64, I64, P], INT),
     "klnmf_solve_exact": ([ctypes.POINTER(SolveArgs), P], INT),
+    "klnmf_kkt_exact": ([ctypes.POINTER(SolveArgs), P, P], INT),
+    "klnmf_mu_update_dev": ([ctypes.POINTER(Side), P, P, P, I32, I32, D, P, I64, P, P], INT),
     "klnmf_solve_fast": ([ctypes.POINTER(SolveArgs), INT, P], INT),
     "klnmf_prepare_fast": ([I32], INT),
     "klnmf_fast_kernel_count": ([], INT),

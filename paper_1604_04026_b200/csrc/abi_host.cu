@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -115,19 +116,25 @@ extern "C" int klnmf_event_record(void *event, void *stream, int external) {
     return 0;
 }
 
-extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
-                                 const double *at, const double *sum_a, double *moving, int64_t j_lo, int64_t j_hi,
-                                 const int64_t *ids, double alpha, double beta, double eps_grad, double eps_x,
-                                 double eps_div, int64_t inner_cap, int64_t r, int64_t n_fix, int64_t n_mov,
-                                 int64_t *stats) {
-    if (r < 1 || n_fix < 0 || n_mov < 0 || j_lo < 0 || j_hi > n_mov)
-        return set_error_msg(1, "klnmf_sweep_range: bad shape or column range");
+// Shared body of the exact host drop-ins: stage the oriented CSC, the fixed
+// factor and the moving columns in the device layout (visit order `ids`),
+// then either solve (max_passes passes) or, with kkt_out, evaluate the KKT
+// violations at the given moving columns; results return in the reference
+// layout.
+static int exact_host_call(const int64_t *col_ptr, const int64_t *row_idx, const double *values, const double *at,
+                           const double *sum_a, double *moving, int64_t j_lo, int64_t j_hi, const int64_t *ids,
+                           double alpha, double beta, double eps_grad, double eps_x, double eps_div,
+                           int64_t inner_cap, int64_t max_passes, int64_t r, int64_t n_fix, int64_t n_mov,
+                           int64_t *stats, double *kkt_out, const char *who) {
+    if (r < 1 || n_fix < 0 || n_mov < 0 || j_lo < 0 || j_hi > n_mov || max_passes < 1)
+        return set_error_msg(1, (std::string(who) + ": bad shape, column range or pass count").c_str());
     if (j_hi <= j_lo) return 0;
     // ids must be a permutation of 0..r-1 (solver.py:287 draws rng.permutation(r))
     std::vector<int32_t> order(r), nat(r, -1);
     for (int64_t t = 0; t < r; ++t) {
-        const int64_t k = ids[t];
-        if (k < 0 || k >= r || nat[k] >= 0) return set_error_msg(1, "klnmf_sweep_range: ids must be a permutation");
+        const int64_t k = ids ? ids[t] : t;
+        if (k < 0 || k >= r || nat[k] >= 0)
+            return set_error_msg(1, (std::string(who) + ": ids must be a permutation").c_str());
         order[t] = (int32_t)k;
         nat[k] = (int32_t)t;
     }
@@ -211,6 +218,20 @@ extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx,
     a.eps_div = eps_div;
     a.inner_cap = inner_cap;
     a.stats = d_stats;
+    a.max_passes = (int32_t)max_passes;
+    if (kkt_out) {
+        double *d_kkt;
+        KLNMF_CHECK(B.alloc(&d_kkt, (int64_t)rp * n_mov));
+        KLNMF_CHECK(cudaMemsetAsync(d_kkt, 0, sizeof(double) * (size_t)rp * (size_t)n_mov, st));
+        rc = klnmf_kkt_exact(&a, d_kkt, st);
+        if (rc) return rc;
+        rc = klnmf_layout_from_device(d_kkt, r, n_mov, d_order, rp, 0, d_mov_ref, st);
+        if (rc) return rc;
+        if (r * n_mov > 0)
+            KLNMF_CHECK(cudaMemcpyAsync(kkt_out, d_mov_ref, sizeof(double) * r * n_mov, cudaMemcpyDeviceToHost, st));
+        KLNMF_CHECK(cudaStreamSynchronize(st));
+        return 0;
+    }
     rc = klnmf_solve_exact(&a, st);
     if (rc) return rc;
     rc = klnmf_layout_from_device(d_moving, r, n_mov, d_order, rp, 0, d_mov_ref, st);
@@ -221,6 +242,97 @@ extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx,
     KLNMF_CHECK(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
     KLNMF_CHECK(cudaStreamSynchronize(st));
     for (int q = 0; q < KLNMF_STATS_LEN; ++q) stats[q] += (int64_t)hs[q];
+    return 0;
+}
+
+extern "C" int klnmf_sweep_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                 const double *at, const double *sum_a, double *moving, int64_t j_lo, int64_t j_hi,
+                                 const int64_t *ids, double alpha, double beta, double eps_grad, double eps_x,
+                                 double eps_div, int64_t inner_cap, int64_t r, int64_t n_fix, int64_t n_mov,
+                                 int64_t *stats) {
+    return exact_host_call(col_ptr, row_idx, values, at, sum_a, moving, j_lo, j_hi, ids, alpha, beta, eps_grad,
+                           eps_x, eps_div, inner_cap, 1, r, n_fix, n_mov, stats, nullptr, "klnmf_sweep_range");
+}
+
+extern "C" int klnmf_sweep_range_passes(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                        const double *at, const double *sum_a, double *moving, int64_t j_lo,
+                                        int64_t j_hi, const int64_t *ids, double alpha, double beta,
+                                        double eps_grad, double eps_x, double eps_div, int64_t inner_cap,
+                                        int64_t max_passes, int64_t r, int64_t n_fix, int64_t n_mov,
+                                        int64_t *stats) {
+    return exact_host_call(col_ptr, row_idx, values, at, sum_a, moving, j_lo, j_hi, ids, alpha, beta, eps_grad,
+                           eps_x, eps_div, inner_cap, max_passes, r, n_fix, n_mov, stats, nullptr,
+                           "klnmf_sweep_range_passes");
+}
+
+extern "C" int klnmf_kkt_violation(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                   const double *at, const double *sum_a, const double *x, double alpha, double beta,
+                                   double eps_grad, double eps_x, double eps_div, int64_t r, int64_t n_fix,
+                                   int64_t n_mov, double *out) {
+    int64_t stats[KLNMF_STATS_LEN] = {0, 0, 0, 0};
+    return exact_host_call(col_ptr, row_idx, values, at, sum_a, const_cast<double *>(x), 0, n_mov, nullptr, alpha,
+                           beta, eps_grad, eps_x, eps_div, 1, 1, r, n_fix, n_mov, stats, out, "klnmf_kkt_violation");
+}
+
+extern "C" int klnmf_mu_update_range(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                                     const double *fixed, double *moving, const double *sum_fixed, double eps_mu,
+                                     int64_t j_lo, int64_t j_hi, int64_t r, int64_t n_fix, int64_t n_mov) {
+    if (r < 1 || n_fix < 0 || n_mov < 0 || j_lo < 0 || j_hi > n_mov)
+        return set_error_msg(1, "klnmf_mu_update_range: bad shape or column range");
+    if (j_hi <= j_lo) return 0;
+    const int64_t nnz = col_ptr[n_mov];
+    if (nnz >= INT32_MAX) return set_error_msg(1, "klnmf_mu_update_range: nnz must be < 2^31");
+    const int32_t rp = round_rp(r);
+    std::vector<int32_t> ident(rp);
+    for (int t = 0; t < rp; ++t) ident[t] = t;
+    std::vector<double> sum_pad(rp, 0.0);
+    for (int64_t k = 0; k < r; ++k) sum_pad[k] = sum_fixed[k];
+    DevBufs B;
+    KLNMF_CHECK(cudaStreamCreateWithFlags(&B.st, cudaStreamNonBlocking));
+    cudaStream_t st = B.st;
+    int64_t *d_ptr, *d_row64;
+    int32_t *d_idx, *d_ident, *d_items;
+    double *d_val, *d_fix_ref, *d_mov_ref, *d_fixed, *d_moving, *d_sum, *d_ratio;
+    KLNMF_CHECK(B.alloc(&d_ptr, n_mov + 1));
+    KLNMF_CHECK(B.alloc(&d_row64, nnz));
+    KLNMF_CHECK(B.alloc(&d_idx, nnz));
+    KLNMF_CHECK(B.alloc(&d_val, nnz));
+    KLNMF_CHECK(B.alloc(&d_ratio, nnz));
+    KLNMF_CHECK(B.alloc(&d_fix_ref, r * n_fix));
+    KLNMF_CHECK(B.alloc(&d_mov_ref, r * n_mov));
+    KLNMF_CHECK(B.alloc(&d_fixed, (int64_t)rp * n_fix));
+    KLNMF_CHECK(B.alloc(&d_moving, (int64_t)rp * n_mov));
+    KLNMF_CHECK(B.alloc(&d_sum, rp));
+    KLNMF_CHECK(B.alloc(&d_ident, rp));
+    KLNMF_CHECK(B.alloc(&d_items, j_hi - j_lo));
+    KLNMF_CHECK(cudaMemcpyAsync(d_ptr, col_ptr, sizeof(int64_t) * (n_mov + 1), cudaMemcpyHostToDevice, st));
+    if (nnz > 0) {
+        KLNMF_CHECK(cudaMemcpyAsync(d_row64, row_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+        KLNMF_CHECK(cudaMemcpyAsync(d_val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+        i64_to_i32<<<grid_for(nnz), 256, 0, st>>>(d_row64, nnz, d_idx);
+        KLNMF_CHECK_LAUNCH("i64_to_i32");
+    }
+    if (r * n_fix > 0)
+        KLNMF_CHECK(cudaMemcpyAsync(d_fix_ref, fixed, sizeof(double) * r * n_fix, cudaMemcpyHostToDevice, st));
+    if (r * n_mov > 0)
+        KLNMF_CHECK(cudaMemcpyAsync(d_mov_ref, moving, sizeof(double) * r * n_mov, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_ident, ident.data(), sizeof(int32_t) * rp, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(cudaMemcpyAsync(d_sum, sum_pad.data(), sizeof(double) * rp, cudaMemcpyHostToDevice, st));
+    iota_from<<<grid_for(j_hi - j_lo), 256, 0, st>>>(d_items, j_hi - j_lo, j_lo);
+    KLNMF_CHECK_LAUNCH("iota_from");
+    int rc = klnmf_layout_to_device(d_fix_ref, r, n_fix, d_ident, rp, d_fixed, 0, st);
+    if (rc) return rc;
+    rc = klnmf_layout_to_device(d_mov_ref, r, n_mov, d_ident, rp, d_moving, 0, st);
+    if (rc) return rc;
+    klnmf_side_t side = {d_ptr, d_idx, d_val, n_fix, n_mov, nnz};
+    rc = klnmf_mu_update_dev(&side, d_fixed, d_moving, d_sum, (int32_t)r, rp, eps_mu, d_items, j_hi - j_lo, d_ratio,
+                             st);
+    if (rc) return rc;
+    rc = klnmf_layout_from_device(d_moving, r, n_mov, d_ident, rp, 0, d_mov_ref, st);
+    if (rc) return rc;
+    if (r * n_mov > 0)
+        KLNMF_CHECK(cudaMemcpyAsync(moving, d_mov_ref, sizeof(double) * r * n_mov, cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(cudaStreamSynchronize(st));
     return 0;
 }
 

@@ -116,11 +116,16 @@ __global__ void __launch_bounds__(EXACT_WPB * 32) solve_exact_kernel(const klnmf
     }
     __syncwarp();
 
-    unsigned long long n_cap = 0, n_deg = 0, n_inner = 0;
+    unsigned long long n_cap = 0, n_deg = 0, n_inner = 0, n_pass = 0;
     const double eg = a.eps_grad;
-    // solve_column body, one pass (_kernels.py:73-118)
-    for (int tt = 0; tt < r; ++tt) {
+    const int max_passes = a.max_passes > 0 ? a.max_passes : 1;
+    // solve_column body (_kernels.py:70-120): passes until one moves nothing
+    for (int pass = 0; pass < max_passes; ++pass) {
+      ++n_pass;
+      bool moved = false;
+      for (int tt = 0; tt < r; ++tt) {
         double x = xs[tt];
+        const double x_enter = x;
         double g, h;
         exact_grad_hess(a, fixed, st, tt, x, &g, &h, lane);
         int64_t inner = 0;
@@ -156,6 +161,9 @@ __global__ void __launch_bounds__(EXACT_WPB * 32) solve_exact_kernel(const klnmf
         __syncwarp();
         if (lane == 0) xs[tt] = x;
         __syncwarp();
+        if (x != x_enter) moved = true;  // warp-uniform: every lane holds the same x
+      }
+      if (!moved) break;
     }
     // moving[:, j] <- x (_kernels.py:143-144), written in the next visit order
     for (int k = lane; k < r; k += 32) moving[j * rp + a.perm_out[k]] = xs[k];
@@ -163,7 +171,86 @@ __global__ void __launch_bounds__(EXACT_WPB * 32) solve_exact_kernel(const klnmf
         if (n_cap) atomicAdd(a.stats + KLNMF_STAT_CAP_HITS, n_cap);
         if (n_deg) atomicAdd(a.stats + KLNMF_STAT_DEGENERATE, n_deg);
         if (n_inner) atomicAdd(a.stats + KLNMF_STAT_INNER_ITERS, n_inner);
-        atomicAdd(a.stats + KLNMF_STAT_PASSES, 1ull);
+        atomicAdd(a.stats + KLNMF_STAT_PASSES, n_pass);
+    }
+}
+
+// kkt_violation (_kernels.py:176-190) of every subproblem at its current x:
+// compute_ax, then per coordinate (natural order) the exact gradient and
+// Hessian diagonal and the reference's violation measure; out is (n_mov, rp)
+// by position.
+__global__ void __launch_bounds__(EXACT_WPB * 32) kkt_exact_kernel(const klnmf_solve_args_t a, double *out) {
+    extern __shared__ double xs_all[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t slot = (int64_t)blockIdx.x * EXACT_WPB + warp;
+    if (slot >= a.n_items) return;
+    const int r = a.r, rp = a.rp;
+    double *xs = xs_all + (int64_t)warp * rp;
+    const double *fixed = static_cast<const double *>(a.fixed);
+    const double *moving = static_cast<const double *>(a.moving);
+    const int64_t j = a.items ? a.items[slot] : slot;
+    const int64_t lo = a.side.ptr[j];
+    ExactState st;
+    st.s = a.side.ptr[j + 1] - lo;
+    st.vi = a.side.idx + lo;
+    st.vv = static_cast<const double *>(a.side.val) + lo;
+    st.t = a.scratch + lo;
+    for (int k = lane; k < r; k += 32) xs[k] = moving[j * rp + a.perm_in[k]];
+    __syncwarp();
+    for (int64_t p = lane; p < st.s; p += 32) {
+        const double *row = fixed + (int64_t)st.vi[p] * rp;
+        double acc = 0.0;
+        for (int k = 0; k < r; ++k) {
+            const int pos = a.nat_pos[k];
+            const double xk = xs[pos];
+            if (xk != 0.0) acc = __dadd_rn(acc, __dmul_rn(xk, __ldg(row + pos)));
+        }
+        st.t[p] = acc;
+    }
+    __syncwarp();
+    const double eg = a.eps_grad;
+    for (int tt = 0; tt < r; ++tt) {
+        const double x = xs[tt];
+        double g, h;
+        exact_grad_hess(a, fixed, st, tt, x, &g, &h, lane);
+        double v;
+        if (x <= eg) {
+            v = fmax(0.0, __dsub_rn(-g, eg));
+        } else {
+            const double scale = fmax(eg, __dmul_rn(__dmul_rn(a.eps_x, x), h));
+            v = fmax(0.0, __dsub_rn(fabs(g), scale));
+        }
+        if (lane == 0) out[j * rp + tt] = v;
+    }
+}
+
+// mu_update_range (_kernels.py:193-214) for every listed subproblem, bit for
+// bit: lanes compute the per-entry data ratios (serial r-dots, natural k
+// order), then each lane owns coordinates and folds the entries in order.
+// Factors are (n, rp) item-major in natural order; ratio is nnz scratch.
+__global__ void __launch_bounds__(EXACT_WPB * 32) mu_exact_kernel(const klnmf_side_t side, const double *fixed,
+                                                                  double *moving, const double *sum_fixed, int r,
+                                                                  int rp, double eps_mu, const int32_t *items,
+                                                                  int64_t n_items, double *ratio) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t slot = (int64_t)blockIdx.x * EXACT_WPB + warp;
+    if (slot >= n_items) return;
+    const int64_t j = items ? items[slot] : slot;
+    const int64_t lo = side.ptr[j], s = side.ptr[j + 1] - lo;
+    const int32_t *idx = side.idx + lo;
+    const double *val = static_cast<const double *>(side.val) + lo;
+    double *mj = moving + j * rp;
+    for (int64_t p = lane; p < s; p += 32) {
+        const double *row = fixed + (int64_t)idx[p] * rp;
+        double d = 0.0;
+        for (int k = 0; k < r; ++k) d = __dadd_rn(d, __dmul_rn(row[k], mj[k]));
+        ratio[lo + p] = __ddiv_rn(val[p], __dadd_rn(d, eps_mu));
+    }
+    __syncwarp();
+    for (int k = lane; k < r; k += 32) {
+        double num = 0.0;
+        for (int64_t p = 0; p < s; ++p) num = __dadd_rn(num, __dmul_rn(fixed[(int64_t)idx[p] * rp + k], ratio[lo + p]));
+        mj[k] = __ddiv_rn(__dmul_rn(mj[k], __dadd_rn(num, eps_mu)), __dadd_rn(sum_fixed[k], eps_mu));
     }
 }
 
@@ -280,6 +367,28 @@ __global__ void sum_partials_kernel(const double *partial, int64_t n, double *ou
 }  // namespace klnmf
 
 using namespace klnmf;
+
+extern "C" int klnmf_kkt_exact(const klnmf_solve_args_t *args, double *out, void *stream) {
+    if (args->n_items <= 0) return 0;
+    const int64_t blocks = (args->n_items + EXACT_WPB - 1) / EXACT_WPB;
+    const size_t smem = sizeof(double) * (size_t)EXACT_WPB * (size_t)args->rp;
+    if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)kkt_exact_kernel, smem));
+    kkt_exact_kernel<<<(unsigned)blocks, EXACT_WPB * 32, smem, as_stream(stream)>>>(*args, out);
+    KLNMF_CHECK_LAUNCH("kkt_exact_kernel");
+    return 0;
+}
+
+extern "C" int klnmf_mu_update_dev(const klnmf_side_t *side, const double *fixed, double *moving,
+                                   const double *sum_fixed, int32_t r, int32_t rp, double eps_mu,
+                                   const int32_t *items, int64_t n_items, double *ratio_scratch, void *stream) {
+    if (n_items <= 0) return 0;
+    const int64_t blocks = (n_items + EXACT_WPB - 1) / EXACT_WPB;
+    mu_exact_kernel<<<(unsigned)blocks, EXACT_WPB * 32, 0, as_stream(stream)>>>(*side, fixed, moving, sum_fixed, r,
+                                                                               rp, eps_mu, items, n_items,
+                                                                               ratio_scratch);
+    KLNMF_CHECK_LAUNCH("mu_exact_kernel");
+    return 0;
+}
 
 extern "C" int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream) {
     if (args->n_items <= 0) return 0;

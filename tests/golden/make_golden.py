@@ -189,8 +189,78 @@ def make_trajectory(name, spec, iters, keep=()):
     print(f"{name}: nnz={V.nnz} {time.time() - t0:.1f}s", flush=True)
 
 
+def _small_matrix(rng, n, m, density):
+    mask = rng.random((n, m)) < density
+    rows, cols = np.nonzero(mask)
+    return klnmf.SparseMatrix.from_coo(n, m, rows, cols, np.round(rng.uniform(0.5, 6.0, size=rows.shape[0])))
+
+
+def make_mu_small():
+    """_kernels.mu_update_range cases (empty columns included) and a short
+    mu_factorize run (multiplicative.py)."""
+    rng = np.random.default_rng(91)
+    cases = []
+    for i in range(20):
+        n_fix, n_mov, r = int(rng.integers(1, 40)), int(rng.integers(1, 30)), int(rng.integers(1, 9))
+        V = _small_matrix(rng, n_fix, n_mov, float(rng.choice([0.05, 0.3, 0.9])))
+        fixed = rng.uniform(0.05, 2.0, size=(r, n_fix))
+        mov = rng.uniform(0.05, 2.0, size=(r, n_mov))
+        sums = klnmf.DenseFactor(fixed).row_sums()
+        eps_mu = float(rng.choice([1e-16, 1e-8]))
+        out = mov.copy()
+        _kernels.mu_update_range(V.col_ptr, V.row_idx, V.values, fixed, out, sums, eps_mu, np.zeros(r), 0, n_mov)
+        cases.append({"col_ptr": V.col_ptr, "row_idx": V.row_idx, "values": V.values, "n_fix": n_fix,
+                      "fixed": fixed, "sum_fixed": sums, "moving_in": mov, "eps_mu": eps_mu, "moving_out": out})
+    save_cases("mu_small.npz", cases)
+    V = klnmf.synthesize(klnmf.SyntheticSpec(n=60, m=80, r_true=3, sparsity=0.8, seed=5))
+    res = klnmf.mu_factorize(V, klnmf.NmfConfig(rank=4, max_outer_iters=12, rel_obj_tol=0.0, seed=6))
+    np.savez_compressed(HERE / "mu_factorize.npz", col_ptr=V.col_ptr, row_idx=V.row_idx, values=V.values,
+                        n_rows=V.n_rows, rank=4, seed=6, iters=12,
+                        kl=np.array(res.log.column("kl_objective")),
+                        total=np.array(res.log.column("total_objective")),
+                        w=res.factors.w.values, f=res.factors.f.values)
+
+
+def make_kkt_small():
+    """subproblem.kkt_violations and multi-pass subproblem.solve_column."""
+    rng = np.random.default_rng(92)
+    kkt, solve = [], []
+    for i in range(16):
+        n_fix, n_mov, r = int(rng.integers(1, 40)), int(rng.integers(1, 12)), int(rng.integers(1, 9))
+        V = _small_matrix(rng, n_fix, n_mov, float(rng.choice([0.1, 0.4, 0.9])))
+        at = rng.uniform(0.0, 2.0, size=(r, n_fix))
+        at[rng.random(at.shape) < 0.3] = 0.0
+        sums = klnmf.DenseFactor(at).row_sums()
+        x = rng.uniform(0.0, 2.0, size=(r, n_mov))
+        x[rng.random(x.shape) < 0.4] = 0.0
+        alpha = float(rng.choice([0.0, 0.1]))
+        beta = float(rng.choice([0.0, 0.05]))
+        tol = klnmf.Tolerances(eps_x=float(rng.choice([0.1, 1e-3])))
+        out = np.stack([klnmf.kkt_violations(V.row_idx[V.col_ptr[j]:V.col_ptr[j + 1]],
+                                             V.values[V.col_ptr[j]:V.col_ptr[j + 1]], at, sums, x[:, j],
+                                             alpha, beta, tol) for j in range(n_mov)], axis=1)
+        kkt.append({"col_ptr": V.col_ptr, "row_idx": V.row_idx, "values": V.values, "n_fix": n_fix, "at": at,
+                    "sum_a": sums, "x": x, "alpha": alpha, "beta": beta, "eps_x": tol.eps_x, "out": out})
+        j = int(rng.integers(0, n_mov))
+        lo, hi = V.col_ptr[j], V.col_ptr[j + 1]
+        ids = rng.permutation(r)
+        max_passes = int(rng.choice([1, 3, 200]))
+        xs, st = klnmf.solve_column(V.row_idx[lo:hi], V.values[lo:hi], at, sums, x[:, j], alpha, beta, ids, tol,
+                                    max_passes=max_passes)
+        solve.append({"v_idx": V.row_idx[lo:hi], "v_val": V.values[lo:hi], "at": at, "sum_a": sums,
+                      "x0": x[:, j], "ids": ids, "alpha": alpha, "beta": beta, "eps_x": tol.eps_x,
+                      "max_passes": max_passes, "x": xs,
+                      "stats": np.array([st.cap_hits, st.degenerate, st.inner_iters, st.passes], dtype=np.int64)})
+    save_cases("kkt_small.npz", kkt)
+    save_cases("solve_column_small.npz", solve)
+
+
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"small", "c1", "c2"}
+    which = set(sys.argv[1:]) or {"small", "c1", "c2", "baselines"}
+    if "baselines" in which:
+        make_mu_small()
+        make_kkt_small()
+        print("baseline fixtures done", flush=True)
     _kernels.warm_up()
     if "small" in which:
         make_sweep_small()

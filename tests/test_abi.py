@@ -37,8 +37,9 @@ def test_fast_kernel_table_is_bucketed():
 def test_struct_layout_matches_header():
     # klnmf_solve_args_t: 6 side fields + 12 pointers/ints, alignment 8
     assert ctypes.sizeof(_lib.Side) == 48
-    # side, 12 pointers, r/rp, 5 doubles, inner_cap, stats, order mode/side, order seed, order_iter
-    assert ctypes.sizeof(_lib.SolveArgs) == 48 + 8 * 12 + 8 + 8 * 5 + 8 + 8 + 8 + 8 + 8
+    # side, 12 pointers, r/rp, 5 doubles, inner_cap, stats, order mode/side, order seed, order_iter,
+    # max_passes/reserved
+    assert ctypes.sizeof(_lib.SolveArgs) == 48 + 8 * 12 + 8 + 8 * 5 + 8 + 8 + 8 + 8 + 8 + 8
 
 
 def test_errors_are_raised_loudly_without_a_device():
