@@ -265,6 +265,19 @@ int klnmf_upload_f64(const double *src_host, int64_t n, double *dst_dev, void *s
 int klnmf_download_f32_as_f64(const float *src_dev, int64_t n, double *dst_host, void *stream);
 int klnmf_download_f64(const double *src_dev, int64_t n, double *dst_host, void *stream);
 
+/* Device-side synthetic corpus (the planted-topic model of synth.py, drawn
+ * with counter-based Philox streams).  Fills col_ptr
+ * (device int64[m+1]), allocates the row indices and values on the device
+ * (values float if fp32, else double) and returns them with nnz; hand them
+ * to caller buffers with klnmf_synth_fetch (which frees them).
+ * length_kind: 0 = Poisson(mean), 1 = lognormal(mean, sigma); zipf <= 0 =
+ * uniform feature popularity. */
+int klnmf_synth_build(uint64_t seed, int64_t n, int64_t m, int32_t topics, double zipf, int length_kind,
+                      double length_mean, double length_sigma, int fp32, int64_t *nnz_out, int64_t *col_ptr,
+                      int32_t **row_idx_out, void **values_out, void *stream);
+int klnmf_synth_fetch(int32_t *rows, void *vals, int64_t nnz, int fp32, int32_t *rows_dst, void *vals_dst,
+                      void *stream);
+
 /* MatrixMarket coordinate files (native reader, the reference's rules and
  * messages, sparse.py:217-268).  klnmf_mm_header reports the size line;
  * klnmf_mm_read fills 0-based int64 rows/cols and fp64 values (nnz_cap >=

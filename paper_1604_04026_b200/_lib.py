@@ -60,6 +60,8 @@ EXPORTS = (
     "klnmf_download_f64",
     "klnmf_mm_header",
     "klnmf_mm_read",
+    "klnmf_synth_build",
+    "klnmf_synth_fetch",
 )
 
 STATS_LEN = 4
@@ -154,6 +156,9 @@ _SIGS = {
     "klnmf_download_f64": ([P, I64, P, P], INT),
     "klnmf_mm_header": ([ctypes.c_char_p, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)], INT),
     "klnmf_mm_read": ([ctypes.c_char_p, I64, P, P, P], INT),
+    "klnmf_synth_build": ([ctypes.c_uint64, I64, I64, I32, D, INT, D, D, INT, ctypes.POINTER(I64), P,
+                           ctypes.POINTER(P), ctypes.POINTER(P), P], INT),
+    "klnmf_synth_fetch": ([P, P, I64, INT, P, P, P], INT),
 }
 
 _lib = None

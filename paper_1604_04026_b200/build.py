@@ -24,7 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
           "-I", str(INCLUDE)]
 # exact mode mirrors the reference's FMA-free numba codegen (SURVEY.md finding 3)
 PER_FILE = {"solve_exact.cu": ["-fmad=false"]}
-SOURCES = ["abi_host.cu", "solve_exact.cu", "solve_fast.cu", "factor_ops.cu", "sparse_build.cu", "host_io.cu", "mm_io.cu"]
+SOURCES = ["abi_host.cu", "solve_exact.cu", "solve_fast.cu", "factor_ops.cu", "sparse_build.cu", "host_io.cu", "mm_io.cu", "synth_gen.cu"]
 
 
 def nvcc() -> str:

@@ -129,14 +129,24 @@ class DevicePlan:
         with torch.cuda.device(dev):
             self.stream_ptr = torch.cuda.current_stream(dev).cuda_stream
             # CSC of V (F-side) uploaded once; CSC of V^T (W-side) built on device
-            csc_ptr = torch.from_numpy(V.col_ptr).to(dev)
-            csc_idx = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
-            csc_val = torch.empty(max(self.nnz, 1), dtype=self.vdt, device=dev)
-            row_idx = np.ascontiguousarray(V.row_idx, dtype=np.int64)
-            values = np.ascontiguousarray(V.values, dtype=np.float64)
-            _lib.call("klnmf_upload_i64_as_i32", row_idx.ctypes.data, self.nnz, csc_idx.data_ptr(), self.stream_ptr)
-            _lib.call("klnmf_upload_f64_as_f32" if self.fp32 else "klnmf_upload_f64", values.ctypes.data,
-                      self.nnz, csc_val.data_ptr(), self.stream_ptr)
+            from .synth import DeviceMatrix
+
+            if isinstance(V, DeviceMatrix):  # already on the device (synth.generate_device)
+                col_ptr_host = V.col_ptr_host
+                csc_ptr = V.col_ptr.to(dev)
+                csc_idx = V.row_idx.to(dev) if self.nnz else torch.empty(1, dtype=torch.int32, device=dev)
+                csc_val = V.values.to(dev, self.vdt) if self.nnz else torch.empty(1, dtype=self.vdt, device=dev)
+            else:
+                col_ptr_host = V.col_ptr
+                csc_ptr = torch.from_numpy(V.col_ptr).to(dev)
+                csc_idx = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+                csc_val = torch.empty(max(self.nnz, 1), dtype=self.vdt, device=dev)
+                row_idx = np.ascontiguousarray(V.row_idx, dtype=np.int64)
+                values = np.ascontiguousarray(V.values, dtype=np.float64)
+                _lib.call("klnmf_upload_i64_as_i32", row_idx.ctypes.data, self.nnz, csc_idx.data_ptr(),
+                          self.stream_ptr)
+                _lib.call("klnmf_upload_f64_as_f32" if self.fp32 else "klnmf_upload_f64", values.ctypes.data,
+                          self.nnz, csc_val.data_ptr(), self.stream_ptr)
             csr_ptr = torch.empty(self.n + 1, dtype=torch.int64, device=dev)
             csr_idx = torch.empty(self.nnz, dtype=torch.int32, device=dev)
             csr_val = torch.empty(self.nnz, dtype=self.vdt, device=dev)
@@ -150,7 +160,7 @@ class DevicePlan:
 
             self.fast_kernels = fast_kernels if fast_kernels is not None else _lib.fast_kernels()
             self.sides = {
-                "F": self._make_side("F", csc_ptr, csc_idx, csc_val, self.n, self.m, V.col_ptr,
+                "F": self._make_side("F", csc_ptr, csc_idx, csc_val, self.n, self.m, col_ptr_host,
                                      map_csc2csr if self.fp32 else None),
                 "W": self._make_side("W", csr_ptr, csr_idx, csr_val, self.m, self.n, csr_ptr_host,
                                      map_csr2csc if self.fp32 else None),

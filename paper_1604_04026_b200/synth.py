@@ -24,7 +24,7 @@ import numpy as np
 from .sparse import SparseMatrix
 from .solver import RegConfig
 
-__all__ = ["ConfigSpec", "CONFIGS", "generate", "generate_coo", "initial_factors"]
+__all__ = ["ConfigSpec", "CONFIGS", "DeviceMatrix", "generate", "generate_coo", "generate_device", "initial_factors"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -135,3 +135,60 @@ def initial_factors(spec: ConfigSpec, round_fp32: bool | None = None):
         w = w.astype(np.float32).astype(np.float64)
         f = f.astype(np.float32).astype(np.float64)
     return w, f
+
+
+@dataclasses.dataclass
+class DeviceMatrix:
+    """A CSC matrix resident on the GPU (col_ptr int64, row_idx int32, values
+    float32/float64 torch tensors), as DevicePlan consumes it -- the C5-scale
+    input never exists in host memory."""
+
+    n_rows: int
+    n_cols: int
+    col_ptr: "object"
+    row_idx: "object"
+    values: "object"
+    col_ptr_host: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_idx.shape[0])
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    def to_host(self) -> SparseMatrix:
+        return SparseMatrix(self.n_rows, self.n_cols, self.col_ptr_host.copy(),
+                            self.row_idx.cpu().numpy().astype(np.int64), self.values.cpu().numpy().astype(np.float64))
+
+
+def generate_device(spec: ConfigSpec, device=None, precision: str | None = None) -> DeviceMatrix:
+    """The config's generative model drawn on the GPU (csrc/synth_gen.cu):
+    same distributions as ``generate``, a different (counter-based) random
+    stream, so a statistically equivalent -- not identical -- matrix."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    precision = precision or spec.precision
+    fp32 = precision == "fp32"
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        col_ptr = torch.empty(spec.m + 1, dtype=torch.int64, device=dev)
+        nnz = ctypes.c_int64()
+        rows_p, vals_p = ctypes.c_void_p(), ctypes.c_void_p()
+        kind = 0 if spec.length[0] == "poisson" else 1
+        sigma = spec.length[2] if kind == 1 else 0.0
+        _lib.call("klnmf_synth_build", int(spec.seed), spec.n, spec.m, spec.topics,
+                  float(spec.zipf) if spec.zipf is not None else 0.0, kind, float(spec.length[1]), float(sigma),
+                  int(fp32), ctypes.byref(nnz), col_ptr.data_ptr(), ctypes.byref(rows_p), ctypes.byref(vals_p),
+                  stream)
+        k = nnz.value
+        rows = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(k, 1), dtype=torch.float32 if fp32 else torch.float64, device=dev)
+        _lib.call("klnmf_synth_fetch", rows_p, vals_p, k, int(fp32), rows.data_ptr(), vals.data_ptr(), stream)
+        return DeviceMatrix(spec.n, spec.m, col_ptr, rows[:k], vals[:k], col_ptr.cpu().numpy())
