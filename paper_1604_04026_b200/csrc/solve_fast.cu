@@ -831,8 +831,9 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const int64_t cn = min(s, c0 + per) - c0;  // entries of this CTA
     const int64_t base = lo + c0;              // global entry index of local entry 0
     const double eps = pm.eps_div;
-    double *Ug = a.scratch + base;  // spilled entries: u and vi in scratch
-    double *VIg = a.scratch + a.side.nnz + base;
+    // spilled entries (rows longer than the on-chip capacity of their CTAs):
+    // (u, vi) interleaved in scratch, one 16-byte access per entry
+    double2 *UVg = reinterpret_cast<double2 *>(a.scratch) + base;
 
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
@@ -867,7 +868,9 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const int64_t spill0 = (int64_t)(NR + NS) * NT;  // first spilled local entry
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const int64_t g = base + i;
-        entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, Ug[i], VIg[i]);
+        double2 uv;
+        entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, uv.x, uv.y);
+        UVg[i] = uv;
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
@@ -908,9 +911,12 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                         accum_from<CC>(red, A[(NR + e) * NT], uu, entry_z(uu, VIs[e * NT + tid]));
                     }
                 });
-                for (int64_t i = spill0 + tid; i < cn; i += NT)
-                    accum_chunk(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), Ug[i],
-                                entry_z(Ug[i], VIg[i]), cc);
+#pragma unroll 4
+                for (int64_t i = spill0 + tid; i < cn; i += NT) {
+                    const double2 uv = __ldcg(UVg + i);
+                    accum_chunk(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), uv.x,
+                                entry_z(uv.x, uv.y), cc);
+                }
                 reduce(red, buf);
                 cur = buf;
                 buf ^= 1;
@@ -951,13 +957,15 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                             }
                             if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
+#pragma unroll 4
                         for (int64_t i = spill0 + tid; i < cn; i += NT) {
                             const double av = (double)__ldg(fixed + (int64_t)a.side.idx[base + i] * rp + tt);
-                            double uu = Ug[i];
-                            const double vv = VIg[i];
+                            double2 uv = __ldcg(UVg + i);
+                            double &uu = uv.x;
+                            const double vv = uv.y;
                             if (upd) {
                                 entry_update<CL>(delta, av, eps, uu, vv);
-                                Ug[i] = uu;
+                                __stcg(UVg + i, uv);
                             }
                             if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
@@ -987,7 +995,10 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     for (int e = 0; e < NS; ++e)
         if (offs[e] >= 0)
             a.t_out[base + tid + (int64_t)(NR + e) * NT] = entry_t(Us[e * NT + tid], VIs[e * NT + tid], eps);
-    for (int64_t i = spill0 + tid; i < cn; i += NT) a.t_out[base + i] = entry_t(Ug[i], VIg[i], eps);
+    for (int64_t i = spill0 + tid; i < cn; i += NT) {
+        const double2 uv = UVg[i];
+        a.t_out[base + i] = entry_t(uv.x, uv.y, eps);
+    }
     flush_stats(cnt, cq == 0 && tid == 0, a.stats, false);
 }
 

@@ -391,3 +391,36 @@ def test_fp32_iterations_per_half_step(cuda_ok, name, m):
             plan.factors[which].copy_(torch.from_numpy(reset))
             plan.t["csc" if which == "F" else "csr"][: plan.nnz].copy_(torch.from_numpy(to))
         ids = nxt
+
+
+def test_coop_spill_beyond_on_chip_capacity(cuda_ok):
+    """A column longer than every CTA's on-chip capacity together, so part of
+    its per-entry state lives in the global spill buffer (C5's longest W-side
+    rows); against the fp32 oracle."""
+    import paper_1604_04026_b200 as kb
+    from paper_1604_04026_b200 import _lib
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    per_cta, n_ctas, _ = _lib.coop_info(8)
+    cap = per_cta * n_ctas
+    rng = np.random.default_rng(12)
+    s_long = cap + cap // 8
+    n = s_long + 1000
+    sizes = [s_long, 70000, 3]
+    rows, cols = [], []
+    for j, s_ in enumerate(sizes):
+        rows.append(np.sort(rng.choice(n, size=s_, replace=False)))
+        cols.append(np.full(s_, j))
+    rows = np.concatenate(rows)
+    V = kb.SparseMatrix.from_coo(n, len(sizes), rows, np.concatenate(cols),
+                                 rng.integers(1, 6, size=rows.shape[0]).astype(np.float64))
+    r = 7
+    w0 = rng.random((r, n)).astype(np.float32).astype(np.float64)
+    w0[rng.random(w0.shape) < 0.3] = 0.0
+    f0 = rng.random((r, len(sizes))).astype(np.float32).astype(np.float64)
+    plan = DevicePlan(V, r, "fp32")
+    ids = rng.permutation(r)
+    plan.set_factors(w0, f0, order=ids)
+    mg, mo, tg, to, sg, so = _compare_half_step(plan, "F", ids, 0.01, 0.0)
+    _check(mg, mo, tg, to, "spill")
+    _check_stats(sg, so)

@@ -40,18 +40,23 @@ out["peak_gb_after_plan"] = torch.cuda.max_memory_allocated() / 1e9
 rng = np.random.default_rng(spec.seed + 1)
 reg = spec.reg
 ms, kls = [], []
+kernels = {}
 for it in range(1, iters + 1):
     nxt = rng.permutation(r)
+    ev = [] if it == iters else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    plan.half_step("F", ids, alpha=reg.alpha2, beta=reg.beta2)
-    plan.half_step("W", ids, nxt, alpha=reg.alpha1, beta=reg.beta1)
+    plan.half_step("F", ids, alpha=reg.alpha2, beta=reg.beta2, events=ev)
+    plan.half_step("W", ids, nxt, alpha=reg.alpha1, beta=reg.beta1, events=ev)
     e1.record()
     torch.cuda.synchronize()
+    for side, kid, a, b in ev or []:
+        kernels[f"{side}:{kid}"] = round(a.elapsed_time(b), 3)
     ids = nxt
     ms.append(e0.elapsed_time(e1))
     kls.append(plan.objective(reg.alpha1, reg.alpha2, reg.beta1, reg.beta2)[1])
 out["ms_per_iteration"] = ms
+out["last_iteration_kernels_ms"] = dict(sorted(kernels.items(), key=lambda kv: -kv[1]))
 out["total_objective"] = kls
 out["updates_per_s_last"] = 2.0 * plan.nnz * r / (ms[-1] * 1e-3)
 out["peak_gb"] = torch.cuda.max_memory_allocated() / 1e9
