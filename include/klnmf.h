@@ -60,6 +60,11 @@ int klnmf_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side
  * CUDA-graph capture a real (timing-capable) event node, re-recorded by every
  * replay (used for per-kernel timing of captured half-steps). */
 int klnmf_event_record(void *event, void *stream, int external);
+/* fork/join plumbing for launching independent buckets on several streams
+ * (captured into one graph): a timing-free event, and stream waits on it */
+int klnmf_event_create(void **event);
+int klnmf_event_destroy(void *event);
+int klnmf_stream_wait(void *stream, void *event);
 
 /* ------------------------------------------------------------------ */
 /* 1. Drop-in host entry points (reference layout, fp64, bit-exact).   */

@@ -26,6 +26,9 @@ EXPORTS = (
     "klnmf_abi_version",
     "klnmf_last_error",
     "klnmf_event_record",
+    "klnmf_event_create",
+    "klnmf_event_destroy",
+    "klnmf_stream_wait",
     "klnmf_chunk_order",
     "klnmf_sweep_range",
     "klnmf_sweep_range_passes",
@@ -122,6 +125,9 @@ _SIGS = {
     "klnmf_abi_version": ([], INT),
     "klnmf_last_error": ([], ctypes.c_char_p),
     "klnmf_event_record": ([P, P, INT], INT),
+    "klnmf_event_create": ([ctypes.POINTER(P)], INT),
+    "klnmf_event_destroy": ([P], INT),
+    "klnmf_stream_wait": ([P, P], INT),
     "klnmf_chunk_order": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, I32, P], INT),
     "klnmf_sweep_range": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, P], INT),
     "klnmf_sweep_range_passes": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, I64, P], INT),

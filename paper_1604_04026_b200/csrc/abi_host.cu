@@ -107,6 +107,23 @@ extern "C" int klnmf_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, ui
     return 0;
 }
 
+extern "C" int klnmf_event_create(void **event) {
+    cudaEvent_t ev;
+    KLNMF_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    *event = ev;
+    return 0;
+}
+
+extern "C" int klnmf_event_destroy(void *event) {
+    if (event) KLNMF_CHECK(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+    return 0;
+}
+
+extern "C" int klnmf_stream_wait(void *stream, void *event) {
+    KLNMF_CHECK(cudaStreamWaitEvent(as_stream(stream), static_cast<cudaEvent_t>(event), 0));
+    return 0;
+}
+
 extern "C" int klnmf_event_record(void *event, void *stream, int external) {
     cudaEvent_t ev = static_cast<cudaEvent_t>(event);
     if (external)

@@ -202,6 +202,10 @@ class DevicePlan:
             self._perm_event = None
             self.use_graphs = True
             self._capturing = False
+            # streams (and fork/join events) for running independent buckets concurrently
+            self._par_streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("KLNMF_PAR_STREAMS", "4")))]
+            self._fork_event = self._new_event()
+            self._join_events = [self._new_event() for _ in self._par_streams]
             if self.fp32:
                 _lib.call("klnmf_prepare_fast", self.rp)
             self._graphs = {}
@@ -209,6 +213,20 @@ class DevicePlan:
             self._pos = torch.zeros(2, self.rp, dtype=torch.int32, device=dev)
 
     # ------------------------------------------------------------------
+    @staticmethod
+    def _new_event():
+        h = ctypes.c_void_p()
+        _lib.call("klnmf_event_create", ctypes.byref(h))
+        return h.value
+
+    def __del__(self):
+        for h in [getattr(self, "_fork_event", None), *getattr(self, "_join_events", [])]:
+            if h:
+                try:
+                    _lib.load().klnmf_event_destroy(h)
+                except Exception:
+                    pass
+
     def _track(self, name, *tensors):
         if self.ledger is not None:
             self.ledger.track(f"dev_{name}", *tensors)
@@ -495,40 +513,55 @@ class DevicePlan:
             a.t_out = self.t["csc" if which == "F" else "csr"].data_ptr()
         item_base = side.items.data_ptr()
         lib = _lib.load()
-        for kid, start, count in side.buckets:
-            if count == 0:
-                continue
+        main = self.stream_ptr
+        buckets = [b for b in side.buckets if b[2] > 0]
+        coop_kid = self._stream_kernel_id()
+        # the cooperative long-row kernel first and alone (it wants every SM);
+        # the other buckets are independent (disjoint outputs, atomic stats)
+        # and fork over several streams, so one bucket's last partial wave and
+        # the few-subproblem buckets overlap the others
+        first = [b for b in buckets if self.fp32 and b[0] == coop_kid]
+        rest = [b for b in buckets if b not in first]
+        n_par = min(len(self._par_streams), len(rest)) if self.fp32 else 0
+        for q, (kid, start, count) in enumerate(first + rest):
+            if q == len(first) and n_par > 1:  # fork
+                _lib.call("klnmf_event_record", self._fork_event, main, 0)
+                for sp in self._par_streams[:n_par]:
+                    _lib.call("klnmf_stream_wait", sp.cuda_stream, self._fork_event)
+            sptr = main if (q < len(first) or n_par <= 1) else self._par_streams[(q - len(first)) % n_par].cuda_stream
             a.items = item_base + 4 * start
             a.n_items = count
-            ev = self._event_pair(events)
+            ev = self._event_pair(events, sptr)
             if not self.fp32:
-                _lib.check(lib.klnmf_solve_exact(ctypes.byref(a), self.stream_ptr), "klnmf_solve_exact")
-            elif kid == self._stream_kernel_id():
+                _lib.check(lib.klnmf_solve_exact(ctypes.byref(a), sptr), "klnmf_solve_exact")
+            elif kid == coop_kid:
                 sched, n_waves, n_ctas, sync, n_groups = side.coop
                 _lib.check(lib.klnmf_solve_coop(ctypes.byref(a), sched.data_ptr(), n_waves, n_ctas,
-                                                sync.data_ptr(), n_groups, self.stream_ptr), "klnmf_solve_coop")
+                                                sync.data_ptr(), n_groups, sptr), "klnmf_solve_coop")
             else:
-                _lib.check(lib.klnmf_solve_fast(ctypes.byref(a), kid, self.stream_ptr), "klnmf_solve_fast")
+                _lib.check(lib.klnmf_solve_fast(ctypes.byref(a), kid, sptr), "klnmf_solve_fast")
             if ev is not None:
-                self._record(ev[1])
+                self._record(ev[1], sptr)
                 events.append((which, kid if self.fp32 else -1, ev[0], ev[1]))
+        if n_par > 1:  # join
+            for i, sp in enumerate(self._par_streams[:n_par]):
+                _lib.call("klnmf_event_record", self._join_events[i], sp.cuda_stream, 0)
+                _lib.call("klnmf_stream_wait", main, self._join_events[i])
 
-    def _event_pair(self, events):
+    def _event_pair(self, events, sptr):
         if events is None:
             return None
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        self._record(e0)
+        self._record(e0, sptr)
         return e0, e1
 
-    def _record(self, ev: torch.cuda.Event) -> None:
-        """Record on the launch stream; inside a graph capture as an external
+    def _record(self, ev: torch.cuda.Event, sptr) -> None:
+        """Record on stream sptr; inside a graph capture as an external
         (timing-capable) event node."""
-        if self._capturing:
+        if ev.cuda_event == 0:
             ev.record(torch.cuda.current_stream(self.dev))  # creates the event handle
-            _lib.call("klnmf_event_record", ev.cuda_event, self.stream_ptr, 1)
-        else:
-            ev.record(torch.cuda.current_stream(self.dev))
+        _lib.call("klnmf_event_record", ev.cuda_event, sptr, 1 if self._capturing else 0)
 
     def _exchange(self, which: str) -> None:
         """All-gather the updated rows of the moving factor (and, in fp32
