@@ -39,6 +39,7 @@ import numpy as np
 import torch
 
 _TIMING = bool(os.environ.get("KLNMF_TIMING"))
+_COOP_PARALLEL = bool(os.environ.get("KLNMF_COOP_PARALLEL"))
 
 from . import _lib
 from .subproblem import SolveStats, Tolerances
@@ -520,7 +521,7 @@ class DevicePlan:
         # the other buckets are independent (disjoint outputs, atomic stats)
         # and fork over several streams, so one bucket's last partial wave and
         # the few-subproblem buckets overlap the others
-        first = [b for b in buckets if self.fp32 and b[0] == coop_kid]
+        first = [b for b in buckets if self.fp32 and b[0] == coop_kid and not _COOP_PARALLEL]
         rest = [b for b in buckets if b not in first]
         n_par = min(len(self._par_streams), len(rest)) if self.fp32 else 0
         for q, (kid, start, count) in enumerate(first + rest):
