@@ -203,7 +203,10 @@ class DevicePlan:
             self._perm_event = None
             self.use_graphs = True
             self._capturing = False
-            # streams (and fork/join events) for running independent buckets concurrently
+            # streams (and fork/join events) for running independent buckets
+            # concurrently; concurrent = False launches them one at a time
+            # (per-kernel timing without overlap)
+            self.concurrent = True
             self._par_streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("KLNMF_PAR_STREAMS", "4")))]
             self._fork_event = self._new_event()
             self._join_events = [self._new_event() for _ in self._par_streams]
@@ -419,7 +422,7 @@ class DevicePlan:
             need = "csr" if which == "F" else "csc"
             if self.t_current != need:
                 self._init_t(need)
-        key = (which, float(alpha), float(beta), tol, dev_sums, events is not None)
+        key = (which, float(alpha), float(beta), tol, dev_sums, events is not None, self.concurrent)
         if self.use_graphs:
             entry = self._graphs.get(key)
             if entry is None:
@@ -456,7 +459,7 @@ class DevicePlan:
         """Capture one side's launch sequence into a CUDA graph.  The fp32
         kernels' one-time launch attributes were set at plan construction
         (klnmf_prepare_fast); the exact mode warms up eagerly once first."""
-        which, alpha, beta, tol, dev_sums, with_events = key
+        which, alpha, beta, tol, dev_sums, with_events, _ = key
         if not self.fp32 and key not in self._warm:
             self._warm.add(key)
             return None  # run eagerly this time
@@ -523,7 +526,7 @@ class DevicePlan:
         # the few-subproblem buckets overlap the others
         first = [b for b in buckets if self.fp32 and b[0] == coop_kid and not _COOP_PARALLEL]
         rest = [b for b in buckets if b not in first]
-        n_par = min(len(self._par_streams), len(rest)) if self.fp32 else 0
+        n_par = min(len(self._par_streams), len(rest)) if (self.fp32 and self.concurrent) else 0
         for q, (kid, start, count) in enumerate(first + rest):
             if q == len(first) and n_par > 1:  # fork
                 _lib.call("klnmf_event_record", self._fork_event, main, 0)
