@@ -192,6 +192,8 @@ int klnmf_prepare_fast(int32_t rp);
 int klnmf_fast_kernel_count(void);
 /* capacity (max nnz per subproblem) and lanes of kernel_id; capacity < 0 = unbounded */
 int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t *lanes, int32_t *npl);
+/* whether kernel_id's shared-memory layout fits the device at padded rank rp */
+int klnmf_fast_kernel_fits(int kernel_id, int32_t rp, int32_t *fits);
 
 /* Long-row bucket (capacity -1 in klnmf_fast_kernel_info): a persistent
  * cooperative kernel, one CTA per SM, each row spread over G CTAs so its

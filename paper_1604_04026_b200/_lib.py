@@ -43,6 +43,7 @@ EXPORTS = (
     "klnmf_prepare_fast",
     "klnmf_fast_kernel_count",
     "klnmf_fast_kernel_info",
+    "klnmf_fast_kernel_fits",
     "klnmf_coop_info",
     "klnmf_solve_coop",
     "klnmf_row_sums_exact",
@@ -142,6 +143,7 @@ _SIGS = {
     "klnmf_prepare_fast": ([I32], INT),
     "klnmf_fast_kernel_count": ([], INT),
     "klnmf_fast_kernel_info": ([INT, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)], INT),
+    "klnmf_fast_kernel_fits": ([INT, I32, ctypes.POINTER(I32)], INT),
     "klnmf_coop_info": ([I32, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I64)], INT),
     "klnmf_solve_coop": ([ctypes.POINTER(SolveArgs), P, I32, I32, P, I64, P], INT),
     "klnmf_row_sums_exact": ([P, I64, I32, I32, P, P], INT),
@@ -209,11 +211,18 @@ def coop_info(rp: int):
     return e.value, n.value, b.value
 
 
-def fast_kernels():
-    """[(kernel_id, capacity, lanes, npl)] of the fp32-mode bucket kernels."""
+def fast_kernels(rp: int | None = None):
+    """[(kernel_id, capacity, lanes, npl)] of the fp32-mode bucket kernels
+    (with rp: only those whose shared-memory layout fits at that padded rank;
+    the long-row kernels always do)."""
     lib = load()
     out = []
     for k in range(lib.klnmf_fast_kernel_count()):
+        if rp is not None:
+            fits = I32()
+            check(lib.klnmf_fast_kernel_fits(k, int(rp), ctypes.byref(fits)), "klnmf_fast_kernel_fits")
+            if not fits.value:
+                continue
         cap, lanes, npl = I64(), I32(), I32()
         check(lib.klnmf_fast_kernel_info(k, ctypes.byref(cap), ctypes.byref(lanes), ctypes.byref(npl)),
               "klnmf_fast_kernel_info")

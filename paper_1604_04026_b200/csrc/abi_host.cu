@@ -20,6 +20,7 @@ static thread_local char g_err[512] = "";
 
 int set_error(cudaError_t err, const char *where) {
     snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorString(err), cudaGetErrorName(err));
+    (void)cudaGetLastError();  // a failed API call must not surface again at the next launch check
     return (int)err;
 }
 

@@ -1088,6 +1088,23 @@ using namespace klnmf;
 
 extern "C" int klnmf_fast_kernel_count(void) { return kNumFast; }
 
+// Dynamic shared memory of a bucket kernel at padded rank rp (counter order:
+// the larger layout); the plan drops kernels that exceed the device limit.
+static size_t fast_kernel_smem(const FastKernel &k, int32_t rp) {
+    if (k.cluster != 0) return slice_smem(rp);
+    return sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt +
+           2 * sizeof(float) * (size_t)k.gpb * (size_t)(rp | 1) + (size_t)k.gpb * MAX_CHUNKS + 16;
+}
+
+extern "C" int klnmf_fast_kernel_fits(int kernel_id, int32_t rp, int32_t *fits) {
+    if (kernel_id < 0 || kernel_id >= kNumFast) return set_error_msg(1, "klnmf_fast_kernel_fits: bad kernel id");
+    int dev = 0, lim = 0;
+    KLNMF_CHECK(cudaGetDevice(&dev));
+    KLNMF_CHECK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    *fits = (rp % 4 == 0 && rp <= KMAX_RP && fast_kernel_smem(kFast[kernel_id], rp) + 8 * 1024 <= (size_t)lim) ? 1 : 0;
+    return 0;
+}
+
 extern "C" int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t *lanes, int32_t *npl) {
     if (kernel_id < 0 || kernel_id >= kNumFast) return set_error_msg(1, "klnmf_fast_kernel_info: bad kernel id");
     *capacity = kFast[kernel_id].capacity;
@@ -1106,8 +1123,12 @@ extern "C" int klnmf_prepare_fast(int32_t rp) {
     if (rp % 4 != 0 || rp > KMAX_RP) return set_error_msg(1, "klnmf_prepare_fast: bad padded rank");
     cudaFuncAttributes fa;
     KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)solve_coop_kernel));  // loads the module now
+    int dev = 0, lim = 0;
+    KLNMF_CHECK(cudaGetDevice(&dev));
+    KLNMF_CHECK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     for (int id = 0; id < kNumFast; ++id) {
         const FastKernel &k = kFast[id];
+        if (fast_kernel_smem(k, rp) + 8 * 1024 > (size_t)lim) continue;  // not used at this rank
         if (k.fn) KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)k.fn));
         if (k.cluster < 0) {
             KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, slice_smem(rp)));

@@ -100,6 +100,8 @@ class DevicePlan:
             raise ValueError("order must be 'shared' or 'counter'")
         if order == "counter" and precision != "fp32":
             raise ValueError("the counter coordinate order is an fp32-mode option (fp64 is the oracle mode)")
+        if precision == "fp32" and round_rp(int(rank)) > 256:
+            raise ValueError("the fp32 mode supports rank <= 256 (use precision='fp64' above that)")
         self.order_mode = _lib.ORDER_COUNTER if order == "counter" else _lib.ORDER_SHARED
         self.order_seed = int(order_seed) & (2**64 - 1)
         if not torch.cuda.is_available():
@@ -159,7 +161,7 @@ class DevicePlan:
                       map_csc2csr.data_ptr(), self.stream_ptr)
             csr_ptr_host = csr_ptr.cpu().numpy()
 
-            self.fast_kernels = fast_kernels if fast_kernels is not None else _lib.fast_kernels()
+            self.fast_kernels = fast_kernels if fast_kernels is not None else _lib.fast_kernels(self.rp)
             self.sides = {
                 "F": self._make_side("F", csc_ptr, csc_idx, csc_val, self.n, self.m, col_ptr_host,
                                      map_csc2csr if self.fp32 else None),
