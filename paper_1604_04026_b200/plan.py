@@ -586,7 +586,8 @@ class DevicePlan:
         if self.world > 1:
             # every rank counted only its own subproblems
             import torch.distributed as dist
-            t = torch.from_numpy(arr.copy()).to(self.dev)
+            nccl = dist.get_backend(self.group) == "nccl"
+            t = torch.from_numpy(arr.copy()).to(self.dev if nccl else "cpu")
             dist.all_reduce(t, group=self.group)
             arr = t.cpu().numpy()
         return SolveStats.from_array(arr)
@@ -645,10 +646,14 @@ def allgather_ranges(buf: torch.Tensor, ranges, group) -> None:
     if maxlen == 0:
         return
     tail = tuple(buf.shape[1:])
-    send = torch.zeros((maxlen,) + tail, dtype=buf.dtype, device=buf.device)
+    # NCCL gathers device memory directly; other backends (gloo: CPU tests,
+    # several ranks sharing one GPU) stage through host memory
+    stage = buf.is_cuda and dist.get_backend(group) != "nccl"
+    dev = torch.device("cpu") if stage else buf.device
+    send = torch.zeros((maxlen,) + tail, dtype=buf.dtype, device=dev)
     lo, hi = ranges[me]
     send[: hi - lo] = buf[lo:hi]
-    recv = torch.empty((world * maxlen,) + tail, dtype=buf.dtype, device=buf.device)
+    recv = torch.empty((world * maxlen,) + tail, dtype=buf.dtype, device=dev)
     dist.all_gather_into_tensor(recv, send, group=group)
     for q, (lo, hi) in enumerate(ranges):
         if q != me and hi > lo:
