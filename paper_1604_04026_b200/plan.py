@@ -39,6 +39,21 @@ import numpy as np
 import torch
 
 _TIMING = bool(os.environ.get("KLNMF_TIMING"))
+
+
+class _Ticker:
+    """Phase wall times (device-synchronised) when KLNMF_TIMING is set."""
+
+    def __init__(self, what):
+        self.what = what
+        self.t = time.perf_counter() if _TIMING else 0.0
+
+    def __call__(self, label):
+        if _TIMING:
+            torch.cuda.synchronize()
+            now = time.perf_counter()
+            print(f"[klnmf] {self.what}: {label} {1e3 * (now - self.t):.1f} ms", flush=True)
+            self.t = now
 _COOP_PARALLEL = bool(os.environ.get("KLNMF_COOP_PARALLEL"))
 
 from . import _lib
@@ -129,6 +144,7 @@ class DevicePlan:
         self.ledger = ledger
         dev = self.dev
 
+        tick = _Ticker("plan")
         with torch.cuda.device(dev):
             self.stream_ptr = torch.cuda.current_stream(dev).cuda_stream
             # CSC of V (F-side) uploaded once; CSC of V^T (W-side) built on device
@@ -155,12 +171,14 @@ class DevicePlan:
             csr_val = torch.empty(self.nnz, dtype=self.vdt, device=dev)
             map_csr2csc = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
             map_csc2csr = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            tick("upload V")
             _lib.call("klnmf_transpose", csc_ptr.data_ptr(), csc_idx.data_ptr(), csc_val.data_ptr(),
                       csc_val.element_size(), self.n, self.m, self.nnz, csr_ptr.data_ptr(),
                       csr_idx.data_ptr(), csr_val.data_ptr(), map_csr2csc.data_ptr(),
                       map_csc2csr.data_ptr(), self.stream_ptr)
             csr_ptr_host = csr_ptr.cpu().numpy()
 
+            tick("transpose")
             self.fast_kernels = fast_kernels if fast_kernels is not None else _lib.fast_kernels(self.rp)
             self.sides = {
                 "F": self._make_side("F", csc_ptr, csc_idx, csc_val, self.n, self.m, col_ptr_host,
@@ -168,9 +186,11 @@ class DevicePlan:
                 "W": self._make_side("W", csr_ptr, csr_idx, csr_val, self.m, self.n, csr_ptr_host,
                                      map_csr2csc if self.fp32 else None),
             }
+            tick("buckets")
             if self.fp32:
                 for sp in self.sides.values():
                     self._build_coop(sp)
+            tick("coop schedule")
             self._track("V_csc", csc_ptr, csc_idx, csc_val)
             self._track("V_csr", csr_ptr, csr_idx, csr_val)
             if self.fp32:
@@ -215,8 +235,10 @@ class DevicePlan:
             if self.fp32:
                 _lib.call("klnmf_prepare_fast", self.rp)
             self._graphs = {}
-            self._warm = set()
+            self._uses = {}
+            self.graph_after = 2  # uses of a half-step key before its launch sequence is captured
             self._pos = torch.zeros(2, self.rp, dtype=torch.int32, device=dev)
+            tick("buffers, prepare")
 
     # ------------------------------------------------------------------
     @staticmethod
@@ -318,7 +340,8 @@ class DevicePlan:
             arr = np.ascontiguousarray(arr, dtype=np.float64)
             if arr.shape != (self.r, n_items):
                 raise ValueError(f"{name} must have shape {(self.r, n_items)}")
-            src = torch.from_numpy(arr).to(self.dev)
+            src = torch.empty(self.r, n_items, dtype=torch.float64, device=self.dev)
+            _lib.call("klnmf_upload_f64", arr.ctypes.data, arr.size, src.data_ptr(), self.stream_ptr)
             o = torch.from_numpy(self._padded(order)).to(self.dev)
             _lib.call("klnmf_layout_to_device", src.data_ptr(), self.r, n_items, o.data_ptr(), self.rp,
                       self.factors[name].data_ptr(), int(self.fp32), self.stream_ptr)
@@ -458,12 +481,16 @@ class DevicePlan:
         self._perm_event.record(torch.cuda.current_stream(self.dev))
 
     def _capture(self, key):
-        """Capture one side's launch sequence into a CUDA graph.  The fp32
+        """Capture one side's launch sequence into a CUDA graph once the key
+        has been used ``graph_after`` times (eager before that: a capture
+        costs tens of ms, which only pays off over many replays).  The fp32
         kernels' one-time launch attributes were set at plan construction
-        (klnmf_prepare_fast); the exact mode warms up eagerly once first."""
+        (klnmf_prepare_fast); the exact mode always warms up eagerly once."""
         which, alpha, beta, tol, dev_sums, with_events, _ = key
-        if not self.fp32 and key not in self._warm:
-            self._warm.add(key)
+        uses = self._uses.get(key, 0) + 1
+        self._uses[key] = uses
+        after = int(os.environ.get("KLNMF_GRAPH_AFTER", self.graph_after))
+        if uses < max(after, 1 if self.fp32 else 2):
             return None  # run eagerly this time
         t_start = time.perf_counter() if _TIMING else 0.0
         graph = torch.cuda.CUDAGraph()

@@ -1,4 +1,6 @@
 """Wall-clock breakdown of factorize() from host arrays (the bench's e2e leg)."""
+import gc
+import os
 import sys
 import time
 from pathlib import Path
@@ -17,6 +19,21 @@ V = synth.generate(spec)
 w0, f0 = synth.initial_factors(spec)
 torch.zeros(1, device="cuda")
 torch.cuda.synchronize()
+
+
+_gc_t0 = [0.0]
+
+
+def _gc_cb(phase, info):
+    if phase == "start":
+        _gc_t0[0] = time.perf_counter()
+    elif time.perf_counter() - _gc_t0[0] > 0.005:
+        print(f"    gc gen{info['generation']} collected {info['collected']} in "
+              f"{1e3 * (time.perf_counter() - _gc_t0[0]):.1f} ms", flush=True)
+
+
+if os.environ.get("E2E_GC_TRACE"):
+    gc.callbacks.append(_gc_cb)
 
 
 def tick(label, t0):
