@@ -41,27 +41,38 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OBJDIR.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str | None = None) -> Path:
+    """variant="phase": a diagnostic copy (libklnmf_phase.so) whose long-row
+    kernels count clock cycles per phase (KLNMF_PHASE_TIMING, tools/phase_timing.py)."""
+    objdir, lib, extra = OBJDIR, LIB, []
+    if variant == "phase":
+        objdir, lib, extra = PKG / "_build_phase", PKG / "libklnmf_phase.so", ["-DKLNMF_PHASE_TIMING"]
+    elif variant is not None:
+        raise ValueError(f"unknown build variant {variant!r}")
+    return _build(objdir, lib, extra, force, verbose)
+
+
+def _build(objdir: Path, lib: Path, extra, force: bool, verbose: bool) -> Path:
+    objdir.mkdir(exist_ok=True)
     headers = [CSRC / "common.cuh", INCLUDE / "klnmf.h"]
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = OBJDIR / (s.stem + ".o")
+        o = objdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers]):
-            cmd = [nvcc(), *ARCH, *COMMON, *PER_FILE.get(src, []), "-c", str(s), "-o", str(o)]
+            cmd = [nvcc(), *ARCH, *COMMON, *extra, *PER_FILE.get(src, []), "-c", str(s), "-o", str(o)]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-pthread", "-o", str(LIB), *map(str, objs)]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-pthread", "-o", str(lib), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True,
+                variant="phase" if "--phase" in sys.argv else None))

@@ -213,6 +213,25 @@ __device__ __forceinline__ void cp_wait() {
 
 __device__ __forceinline__ float comp(const float4 *p, int c) { return reinterpret_cast<const float *>(p)[c]; }
 
+// xs[k] = moving row j at visit position k, for k = first, first + step, ...
+// (pin: the visit-order map staged in shared memory).  Four loads are issued
+// before their stores, so a subproblem's start costs one load latency, not
+// one per position.
+__device__ __forceinline__ void load_row(float *xs, const float *row, const int *pin, int r, int first, int step,
+                                         bool valid) {
+    for (int k0 = first; k0 < r; k0 += 4 * step) {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k = k0 + i * step;
+            v[i] = (valid && k < r) ? row[pin[k]] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (k0 + i * step < r) xs[k0 + i * step] = v[i];
+    }
+}
+
 // Transposed reduction of NV values across the L lanes of a group: after it
 // each lane holds KEEP totals; lanes whose low (NL-HL) bits are zero hold
 // distinct totals, indices (gl >> (NL-HL)) * KEEP + s.
@@ -273,6 +292,44 @@ __device__ __forceinline__ void flush_stats(const Counters &cnt, bool lead, unsi
     if (cp) atomicAdd(stats + KLNMF_STAT_PASSES, (unsigned long long)cp);
 }
 
+// Diagnostic build only (build.py variant "phase", tools/phase_timing.py):
+// clock cycles per phase of the long-row kernels, thread 0 of every CTA,
+// [kind][slot], kind 0 = cluster, 1 = cooperative, 2 = warp kernels (lane 0
+// of every warp).  Slots 0-7 are cycles
+// (init, gather, pass, chunk reduction, scalar Newton, update/re-evaluation,
+// re-evaluation reduction, final writes), 8-11 counts (chunk reductions,
+// re-evaluation reductions, moves, chunks).
+#ifdef KLNMF_PHASE_TIMING
+__device__ unsigned long long g_phase[3][16];
+__device__ __forceinline__ long long phase_now() {
+    long long n;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(n));
+    return n;
+}
+struct PhaseClock {
+    long long t, acc[16];
+    __device__ PhaseClock() : t(phase_now()) {
+        for (int i = 0; i < 16; ++i) acc[i] = 0;
+    }
+    __device__ __forceinline__ void mark(int i) {
+        const long long n = phase_now();
+        acc[i] += n - t;
+        t = n;
+    }
+    __device__ __forceinline__ void count(int i) { ++acc[i]; }
+    __device__ void flush(int kind, bool lead) {
+        if (lead)
+            for (int i = 0; i < 16; ++i) atomicAdd(&g_phase[kind][i], (unsigned long long)acc[i]);
+    }
+};
+#else
+struct PhaseClock {
+    __device__ __forceinline__ void mark(int) {}
+    __device__ __forceinline__ void count(int) {}
+    __device__ __forceinline__ void flush(int, bool) {}
+};
+#endif
+
 // ---------------------------------------------------------------------------
 // Warp kernel: groups of L <= 32 lanes, 32/L subproblems per warp in lock-step.
 template <int L, int NPL>
@@ -286,6 +343,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     // counter order only: [GPB][MAX_CHUNKS] visit order of each group's chunks
     uint8_t *cord_all = reinterpret_cast<uint8_t *>(xs_all + GPB * 2 * (a.rp | 1));
     __shared__ double ssum[KMAX_RP];  // fixed-factor row sums by position
+    __shared__ int pin[KMAX_RP];      // visit position -> stored position (perm_in)
     __shared__ double tots[GPB][NV];  // reduced partial sums of each group
 
     const int tid = threadIdx.x;
@@ -299,10 +357,14 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     double *tot = tots[grp];
     const int64_t slot = (int64_t)blockIdx.x * GPB + grp;
     const bool valid = slot < a.n_items;
-    for (int k = tid; k < r; k += NT) ssum[k] = a.sum_pos[k];
+    for (int k = tid; k < r; k += NT) {
+        ssum[k] = a.sum_pos[k];
+        pin[k] = a.perm_in[k];
+    }
     __syncthreads();
     if (!__any_sync(FULL_MASK, valid)) return;
 
+    PhaseClock ph;
     const Params pm(a);
     const float *fixed = static_cast<const float *>(a.fixed);
     float *moving = static_cast<float *>(a.moving);
@@ -311,7 +373,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     const int64_t lo = valid ? a.side.ptr[j] : 0;
     const int s = valid ? (int)(a.side.ptr[j + 1] - lo) : 0;
 
-    for (int k = gl; k < r; k += L) xs[k] = valid ? moving[j * rp + a.perm_in[k]] : 0.f;
+    load_row(xs, moving + j * rp, pin, r, gl, L, valid);
     const int nchunks = (r + C - 1) / C;
     const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
     uint8_t *cord = cord_all + grp * MAX_CHUNKS;
@@ -347,11 +409,14 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) issue(st);
     __syncwarp();
+    ph.mark(0);
 
     Counters cnt;
     for (int ch = 0; ch < nchunks; ++ch) {
+        ph.count(11);
         issue(ch + STAGES - 1);
         cp_wait<STAGES - 1>();
+        ph.mark(1);
         const float4 *Ach = ring + (ch % STAGES) * NPL * NT + tid;  // own slots of this stage
         const int pc = phys(ch);  // per group in counter order
         const int nc = counter ? C : min(C, r - ch * C);
@@ -369,9 +434,12 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                     for (int e = 0; e < NPL; ++e)
                         accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], entry_z(u[e], vi[e]));
                 });
+                ph.mark(2);
                 TReduce<L>::run(red, gl);
                 TReduce<L>::store(red, gl, tot);
                 __syncwarp();
+                ph.mark(3);
+                ph.count(8);
                 fresh = true;
             }
             double x = (double)xs[tt];
@@ -385,6 +453,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 bool again = false;
                 double delta = 0.0;
                 if (active) delta = newton_step(g, h, x, inner, active, again, pm, cnt);
+                ph.mark(4);
                 if (__any_sync(FULL_MASK, delta != 0.0)) {
                     if (delta != 0.0) moved = true;
                     // delta == 0 (groups not moving) leaves every entry unchanged (q = 1)
@@ -394,6 +463,8 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                             entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, cc)), pm.eps_div, u[e],
                                                               vi[e]);
                     });
+                    ph.mark(5);
+                    ph.count(10);
                 }
                 if (__any_sync(FULL_MASK, again)) {
                     double g2 = 0.0, h2 = 0.0;
@@ -410,10 +481,13 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                         h = pm.alpha + h2;
                         active = enters(g, x, pm.eps_grad);
                     }
+                    ph.mark(6);
+                    ph.count(9);
                 }
             }
             if (moved) fresh = false;
             if (gl == 0 && valid && live) xo[tt] = (float)x;
+            ph.mark(4);
         }
     }
     cp_wait<0>();
@@ -425,6 +499,8 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
             if (gl + e * L < s) a.t_out[lo + gl + e * L] = entry_t(u[e], vi[e], pm.eps_div);
     }
     flush_stats(cnt, gl == 0 && valid, a.stats, true);
+    ph.mark(7);
+    ph.flush(2, (threadIdx.x & 31) == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -817,6 +893,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     float *xo = xs + (a.rp | 1);
     uint8_t *cord = reinterpret_cast<uint8_t *>(xo + (a.rp | 1));  // counter order
 
+    PhaseClock ph;
     const Params pm(a);
     const int tid = threadIdx.x;
     const int rp = a.rp, r = a.r;
@@ -877,10 +954,12 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
     if (counter && tid == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
     __syncthreads();
+    ph.mark(0);
 
     Counters cnt;
     int buf = 0, cur = 0;
     for (int ch = 0; ch < nchunks; ++ch) {
+        ph.count(11);
         const int pc = counter ? (int)cord[ch] : ch;  // physical chunk
         // gather this chunk of every resident entry once (own slots only)
 #pragma unroll
@@ -891,6 +970,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + pc * C, offs[e] >= 0);
         cp_commit();
         cp_wait<0>();
+        ph.mark(1);
         const float4 *A = cache + tid;
         const int nc = min(C, r - pc * C);
         bool fresh = false;
@@ -917,7 +997,10 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                     accum_chunk(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), uv.x,
                                 entry_z(uv.x, uv.y), cc);
                 }
+                ph.mark(2);
                 reduce(red, buf);
+                ph.mark(3);
+                ph.count(8);
                 cur = buf;
                 buf ^= 1;
                 fresh = true;
@@ -932,6 +1015,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             while (active) {  // uniform over the group
                 bool again = false;
                 const double delta = newton_step(g, h, x, inner, active, again, pm, cnt);
+                ph.mark(4);
                 const bool upd = delta != 0.0;  // uniform over the group
                 if (upd) moved = true;
                 double g2 = 0.0, h2 = 0.0;
@@ -970,10 +1054,14 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                             if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
                     });
+                    ph.mark(5);
+                    if (upd) ph.count(10);
                 }
                 if (again) {
                     double ev[NV] = {g2, h2};
                     reduce(ev, buf);
+                    ph.mark(6);
+                    ph.count(9);
                     g = (sb + pm.alpha * x) - R.tot[buf][0];
                     h = pm.alpha + R.tot[buf][1];
                     buf ^= 1;
@@ -983,6 +1071,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             }
             if (moved) fresh = false;
             if (tid == 0) xo[tt] = (float)x;
+            ph.mark(4);
         }
     }
     __syncthreads();
@@ -1000,6 +1089,8 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         a.t_out[base + i] = entry_t(uv.x, uv.y, eps);
     }
     flush_stats(cnt, cq == 0 && tid == 0, a.stats, false);
+    ph.mark(7);
+    ph.flush(std::is_same<Reducer, CoopReducer>::value ? 1 : 0, threadIdx.x == 0);
 }
 
 __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_cluster_kernel(const klnmf_solve_args_t a) {
@@ -1084,12 +1175,29 @@ inline size_t slice_smem(int rp) {
 }  // namespace
 }  // namespace klnmf
 
+#ifdef KLNMF_PHASE_TIMING
+// diagnostic build only: copies out (and optionally clears) the phase counters
+extern "C" int klnmf_debug_phase(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, klnmf::g_phase, sizeof(klnmf::g_phase)) != cudaSuccess) return 1;
+    if (reset) {
+        static const unsigned long long zero[3][16] = {};
+        if (cudaMemcpyToSymbol(klnmf::g_phase, zero, sizeof(zero)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+#endif
+
 using namespace klnmf;
 
 extern "C" int klnmf_fast_kernel_count(void) { return kNumFast; }
 
 // Dynamic shared memory of a bucket kernel at padded rank rp (counter order:
 // the larger layout); the plan drops kernels that exceed the device limit.
+// Dynamic shared memory above which a launch opts in to the large carve-out:
+// static + dynamic must stay within 48 KB without it, and the kernels' static
+// shared memory (row sums, visit map, per-group sums) reaches ~11 KB.
+constexpr size_t SMEM_OPTIN = 32 * 1024;
+
 static size_t fast_kernel_smem(const FastKernel &k, int32_t rp) {
     if (k.cluster != 0) return slice_smem(rp);
     return sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt +
@@ -1142,7 +1250,7 @@ extern "C" int klnmf_prepare_fast(int32_t rp) {
             const size_t smem = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries *
                                     (size_t)k.nt +
                                 2 * sizeof(float) * (size_t)k.gpb * (size_t)(rp | 1) + (size_t)k.gpb * MAX_CHUNKS + 16;
-            if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
+            if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
         }
     }
     return 0;
@@ -1186,7 +1294,7 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     const size_t ring = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt;
     const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) +
                         (args->order_mode != KLNMF_ORDER_SHARED ? (size_t)k.gpb * MAX_CHUNKS : 0) + 16;
-    if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
+    if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
     k.fn<<<(unsigned)blocks, k.nt, smem, as_stream(stream)>>>(*args);
     KLNMF_CHECK_LAUNCH("klnmf_solve_fast");
     return 0;

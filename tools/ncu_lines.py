@@ -15,8 +15,11 @@ from ncu_sass_top import load, num  # noqa: E402
 def disasm_lines(obj, func_sub):
     tmp = Path(tempfile.mkdtemp())
     subprocess.run(["cuobjdump", "-xelf", "all", str(Path(obj).resolve())], cwd=tmp, capture_output=True)
-    cubin = next(tmp.glob("*.cubin"))
-    out = subprocess.run(["nvdisasm", "-g", "-c", str(cubin)], capture_output=True, text=True).stdout
+    out = ""
+    for cubin in sorted(tmp.glob("*.cubin")):  # the object holding the function
+        out = subprocess.run(["nvdisasm", "-g", "-c", str(cubin)], capture_output=True, text=True).stdout
+        if func_sub in out:
+            break
     lines, cur, infn = [], None, False
     for l in out.splitlines():
         if l.startswith(".text.") or re.match(r"^\s*\.section\s+\.text\.", l):
