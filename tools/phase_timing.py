@@ -1,12 +1,13 @@
-"""Per-phase clock cycles of the long-row kernels (cluster, cooperative) on a
-steady-state iteration, from the diagnostic build
+"""Per-phase clock cycles of the solver kernels (cluster, cooperative, warp)
+on steady-state iterations, from the diagnostic build
 (``python -m paper_1604_04026_b200.build --phase`` -> libklnmf_phase.so).
 
     python tools/phase_timing.py [cfg] [warm_iters] [timed_iters]
 
-Thread 0 of every CTA (lane 0 of every warp for the warp kernels) accumulates the cycles between phase marks of
-solve_slice; the table gives each phase's share of CTA time and its mean per
-event (cycles per chunk reduction, per re-evaluation reduction, per move).
+Thread 0 of every cluster / cooperative CTA and lane 0 of every warp-kernel
+warp accumulate the cycles between phase marks; the table gives each phase's
+share of that time and its mean per event (cycles per chunk reduction, per
+re-evaluation reduction, per move).
 """
 import ctypes
 import os
