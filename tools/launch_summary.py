@@ -25,10 +25,15 @@ def main(path):
         v = float(r[vi].replace(",", ""))
         v = v / 1e6 if r[ui] == "ns" else (v / 1e3 if r[ui] in ("us", "usecond") else v)
         launches.append((r[ki], r[gi], r[bi], v))
-    # the timed interval of the last step starts after bench.py's device sleep
-    # (spin_kernel) and ends at the stats read-back (FillFunctor<long>)
+    # the last timed step starts after bench.py's device sleep (spin_kernel)
+    # and ends at the next fill (stats reset / L2 flush of what follows:
+    # bench.py's serialised instrumented pass)
     last = max(i for i, l in enumerate(launches) if "spin_kernel" in l[0])
-    step = [l for l in launches[last + 1:] if "FillFunctor<long>" not in l[0]]
+    step = []
+    for l in launches[last + 1:]:
+        if "FillFunctor" in l[0]:
+            break
+        step.append(l)
     tot = sum(l[3] for l in step)
     agg = OrderedDict()
     for name, grid, block, ms in step:
