@@ -65,6 +65,14 @@ int klnmf_event_record(void *event, void *stream, int external);
 int klnmf_event_create(void **event);
 int klnmf_event_destroy(void *event);
 int klnmf_stream_wait(void *stream, void *event);
+/* CUDA IPC for the fused sharded exchange (klnmf_solve_args_t.peer_*):
+ * export the device allocation holding ptr as a 64-byte handle plus ptr's
+ * byte offset inside it; open a peer process's handle (returns the mapped
+ * base of its allocation, peer access enabled lazily over NVLink); close a
+ * mapped base. */
+int klnmf_ipc_export(const void *ptr, void *handle, int64_t *offset);
+int klnmf_ipc_open(const void *handle, void **base);
+int klnmf_ipc_close(void *base);
 
 /* ------------------------------------------------------------------ */
 /* 1. Drop-in host entry points (reference layout, fp64, bit-exact).   */
@@ -166,7 +174,15 @@ typedef struct {
      * one moves nothing (solve_column's max_passes, _kernels.py:70-120);
      * 0 or 1 = the single pass of sweep_range */
     int32_t max_passes;
-    int32_t reserved0;
+    /* fp32 mode, fused exchange of a sharded run: the kernels also store every
+     * result they write -- moving rows and maintained products of this rank's
+     * subproblems -- into the n_peers other ranks' copies (device arrays of
+     * peer base pointers, same layout as moving / t_out, mapped through CUDA
+     * IPC over NVLink), so no all-gather follows the half-step.  0 = local
+     * writes only. */
+    int32_t n_peers;
+    void *const *peer_moving;
+    double *const *peer_t;
 } klnmf_solve_args_t;
 
 #define KLNMF_ORDER_SHARED 0

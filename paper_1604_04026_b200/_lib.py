@@ -29,6 +29,9 @@ EXPORTS = (
     "klnmf_event_create",
     "klnmf_event_destroy",
     "klnmf_stream_wait",
+    "klnmf_ipc_export",
+    "klnmf_ipc_open",
+    "klnmf_ipc_close",
     "klnmf_chunk_order",
     "klnmf_sweep_range",
     "klnmf_sweep_range_passes",
@@ -118,7 +121,9 @@ class SolveArgs(ctypes.Structure):
         ("order_seed", ctypes.c_uint64),
         ("order_iter", P),
         ("max_passes", I32),
-        ("reserved0", I32),
+        ("n_peers", I32),
+        ("peer_moving", P),
+        ("peer_t", P),
     ]
 
 
@@ -129,6 +134,9 @@ _SIGS = {
     "klnmf_event_create": ([ctypes.POINTER(P)], INT),
     "klnmf_event_destroy": ([P], INT),
     "klnmf_stream_wait": ([P, P], INT),
+    "klnmf_ipc_export": ([P, P, ctypes.POINTER(I64)], INT),
+    "klnmf_ipc_open": ([P, ctypes.POINTER(P)], INT),
+    "klnmf_ipc_close": ([P], INT),
     "klnmf_chunk_order": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, I32, P], INT),
     "klnmf_sweep_range": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, P], INT),
     "klnmf_sweep_range_passes": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, I64, P], INT),

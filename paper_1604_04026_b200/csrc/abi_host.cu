@@ -120,6 +120,45 @@ extern "C" int klnmf_event_destroy(void *event) {
     return 0;
 }
 
+// --- CUDA IPC (fused sharded exchange) ---
+// The allocation base of a device pointer comes from the driver's
+// cuMemGetAddressRange, reached through the runtime's entry-point query so the
+// library needs no link-time libcuda.
+typedef int (*GetAddressRangeFn)(unsigned long long *base, size_t *size, unsigned long long ptr);
+
+extern "C" int klnmf_ipc_export(const void *ptr, void *handle, int64_t *offset) {
+    static GetAddressRangeFn range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        KLNMF_CHECK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn)
+            return set_error_msg(1, "klnmf_ipc_export: cuMemGetAddressRange is not available");
+        range = reinterpret_cast<GetAddressRangeFn>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0)
+        return set_error_msg(1, "klnmf_ipc_export: not a device allocation");
+    cudaIpcMemHandle_t h;
+    KLNMF_CHECK(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+    memcpy(handle, &h, sizeof(h));
+    *offset = (int64_t)((unsigned long long)(uintptr_t)ptr - base);
+    return 0;
+}
+
+extern "C" int klnmf_ipc_open(const void *handle, void **base) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    KLNMF_CHECK(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+    return 0;
+}
+
+extern "C" int klnmf_ipc_close(void *base) {
+    if (base) KLNMF_CHECK(cudaIpcCloseMemHandle(base));
+    return 0;
+}
+
 extern "C" int klnmf_stream_wait(void *stream, void *event) {
     KLNMF_CHECK(cudaStreamWaitEvent(as_stream(stream), static_cast<cudaEvent_t>(event), 0));
     return 0;

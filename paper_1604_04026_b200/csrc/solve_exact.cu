@@ -394,6 +394,8 @@ extern "C" int klnmf_solve_exact(const klnmf_solve_args_t *args, void *stream) {
     if (args->n_items <= 0) return 0;
     if (args->order_mode != KLNMF_ORDER_SHARED)
         return set_error_msg(1, "klnmf_solve_exact: the exact mode visits the shared (reference) order only");
+    if (args->n_peers != 0)
+        return set_error_msg(1, "klnmf_solve_exact: the fused peer exchange is an fp32-mode path (exact mode all-gathers)");
     const int64_t blocks = (args->n_items + EXACT_WPB - 1) / EXACT_WPB;
     const size_t smem = sizeof(double) * (size_t)EXACT_WPB * (size_t)args->rp;
     if (smem > 48 * 1024) KLNMF_CHECK(ensure_smem((const void *)solve_exact_kernel, smem));

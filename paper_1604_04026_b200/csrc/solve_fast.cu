@@ -273,6 +273,19 @@ struct TReduce {
     }
 };
 
+// A result of this rank's subproblems (a moving-factor value, a maintained
+// product): stored locally and, in a fused sharded exchange, into every
+// peer's copy through its CUDA-IPC mapping (NVLink stores issued as the
+// results are produced) -- no all-gather follows the half-step.
+__device__ __forceinline__ void put_moving(const klnmf_solve_args_t &a, float *moving, int64_t i, float v) {
+    moving[i] = v;
+    for (int p = 0; p < a.n_peers; ++p) static_cast<float *>(a.peer_moving[p])[i] = v;
+}
+__device__ __forceinline__ void put_t(const klnmf_solve_args_t &a, int64_t i, double v) {
+    a.t_out[i] = v;
+    for (int p = 0; p < a.n_peers; ++p) a.peer_t[p][i] = v;
+}
+
 __device__ __forceinline__ void flush_stats(const Counters &cnt, bool lead, unsigned long long *stats, bool warp_sum) {
     if (!stats) return;
     unsigned ci = lead ? cnt.n_inner : 0u, cc = lead ? cnt.n_cap : 0u, cd = lead ? cnt.n_deg : 0u;
@@ -298,7 +311,8 @@ __device__ __forceinline__ void flush_stats(const Counters &cnt, bool lead, unsi
 // of every warp).  Slots 0-7 are cycles
 // (init, gather, pass, chunk reduction, scalar Newton, update/re-evaluation,
 // re-evaluation reduction, final writes), 8-11 counts (chunk reductions,
-// re-evaluation reductions, moves, chunks).
+// re-evaluation reductions, moves, chunks), 12 the cycles of each subproblem's
+// first reduction (which also waits for the slowest CTA of the group to arrive).
 #ifdef KLNMF_PHASE_TIMING
 __device__ unsigned long long g_phase[3][16];
 __device__ __forceinline__ long long phase_now() {
@@ -493,10 +507,10 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     cp_wait<0>();
     __syncwarp();
     if (valid) {
-        for (int k = gl; k < r; k += L) moving[j * rp + a.perm_out[k]] = xo[k];
+        for (int k = gl; k < r; k += L) put_moving(a, moving, j * rp + a.perm_out[k], xo[k]);
 #pragma unroll
         for (int e = 0; e < NPL; ++e)
-            if (gl + e * L < s) a.t_out[lo + gl + e * L] = entry_t(u[e], vi[e], pm.eps_div);
+            if (gl + e * L < s) put_t(a, lo + gl + e * L, entry_t(u[e], vi[e], pm.eps_div));
     }
     flush_stats(cnt, gl == 0 && valid, a.stats, true);
     ph.mark(7);
@@ -663,10 +677,10 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     }
     cp_wait<0>();
     __syncthreads();
-    for (int k = tid; k < r; k += NT) moving[j * rp + a.perm_out[k]] = xo[k];
+    for (int k = tid; k < r; k += NT) put_moving(a, moving, j * rp + a.perm_out[k], xo[k]);
 #pragma unroll
     for (int e = 0; e < NPL; ++e)
-        if (tid + e * NT < s) a.t_out[lo + tid + e * NT] = entry_t(u[e], vi[e], pm.eps_div);
+        if (tid + e * NT < s) put_t(a, lo + tid + e * NT, entry_t(u[e], vi[e], pm.eps_div));
     flush_stats(cnt, tid == 0, a.stats, false);
 }
 
@@ -999,7 +1013,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                 }
                 ph.mark(2);
                 reduce(red, buf);
-                ph.mark(3);
+                ph.mark(ch == 0 && cc == 0 ? 12 : 3);  // a job's first reduction also waits for its partners
                 ph.count(8);
                 cur = buf;
                 buf ^= 1;
@@ -1076,17 +1090,17 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     }
     __syncthreads();
     if (cq == 0)
-        for (int kk = tid; kk < r; kk += NT) moving[j * rp + a.perm_out[kk]] = xo[kk];
+        for (int kk = tid; kk < r; kk += NT) put_moving(a, moving, j * rp + a.perm_out[kk], xo[kk]);
 #pragma unroll
     for (int e = 0; e < NR; ++e)
-        if (off[e] >= 0) a.t_out[base + tid + (int64_t)e * NT] = entry_t(u[e], vi[e], eps);
+        if (off[e] >= 0) put_t(a, base + tid + (int64_t)e * NT, entry_t(u[e], vi[e], eps));
 #pragma unroll
     for (int e = 0; e < NS; ++e)
         if (offs[e] >= 0)
-            a.t_out[base + tid + (int64_t)(NR + e) * NT] = entry_t(Us[e * NT + tid], VIs[e * NT + tid], eps);
+            put_t(a, base + tid + (int64_t)(NR + e) * NT, entry_t(Us[e * NT + tid], VIs[e * NT + tid], eps));
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const double2 uv = UVg[i];
-        a.t_out[base + i] = entry_t(uv.x, uv.y, eps);
+        put_t(a, base + i, entry_t(uv.x, uv.y, eps));
     }
     flush_stats(cnt, cq == 0 && tid == 0, a.stats, false);
     ph.mark(7);
@@ -1264,6 +1278,8 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
         return set_error_msg(1, "klnmf_solve_fast: bad coordinate order mode");
     if (!(args->eps_div > 0.0)) return set_error_msg(1, "klnmf_solve_fast: the fp32 mode needs eps_div > 0");
+    if (args->n_peers < 0 || (args->n_peers > 0 && (!args->peer_moving || !args->peer_t)))
+        return set_error_msg(1, "klnmf_solve_fast: n_peers > 0 needs both peer pointer arrays");
     const FastKernel &k = kFast[kernel_id];
     if (k.cluster < 0) return set_error_msg(1, "klnmf_solve_fast: the long-row bucket runs through klnmf_solve_coop");
     if (k.cluster > 0) {
@@ -1321,6 +1337,8 @@ extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *sche
     if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
         return set_error_msg(1, "klnmf_solve_coop: bad coordinate order mode");
     if (!(args->eps_div > 0.0)) return set_error_msg(1, "klnmf_solve_coop: the fp32 mode needs eps_div > 0");
+    if (args->n_peers < 0 || (args->n_peers > 0 && (!args->peer_moving || !args->peer_t)))
+        return set_error_msg(1, "klnmf_solve_coop: n_peers > 0 needs both peer pointer arrays");
     cudaStream_t st = as_stream(stream);
     const size_t smem = slice_smem(args->rp);
     KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, smem));

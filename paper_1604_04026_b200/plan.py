@@ -108,7 +108,8 @@ class SidePlan:
 
 class DevicePlan:
     def __init__(self, V, rank: int, precision: str = "fp64", device=None, group=None,
-                 ledger=None, fast_kernels: list | None = None, order: str = "shared", order_seed: int = 0):
+                 ledger=None, fast_kernels: list | None = None, order: str = "shared", order_seed: int = 0,
+                 fused_exchange: bool | None = None):
         if precision not in ("fp64", "fp32"):
             raise ValueError("precision must be 'fp64' or 'fp32'")
         if order not in ("shared", "counter"):
@@ -239,6 +240,15 @@ class DevicePlan:
             self.graph_after = 2  # uses of a half-step key before its launch sequence is captured
             self._pos = torch.zeros(2, self.rp, dtype=torch.int32, device=dev)
             tick("buffers, prepare")
+            # sharded fp32 runs exchange results inside the kernels (peer
+            # stores through CUDA IPC) unless disabled; fp64 all-gathers
+            self._peers = None
+            self._ipc_bases = []
+            if fused_exchange is None:
+                fused_exchange = os.environ.get("KLNMF_FUSED_EXCHANGE", "1") != "0"
+            if self.world > 1 and self.fp32 and fused_exchange:
+                self._setup_peers()
+                tick("peer mappings")
 
     # ------------------------------------------------------------------
     @staticmethod
@@ -254,6 +264,71 @@ class DevicePlan:
                     _lib.load().klnmf_event_destroy(h)
                 except Exception:
                     pass
+        bases = getattr(self, "_ipc_bases", [])
+        if bases:
+            try:
+                torch.cuda.synchronize(self.dev)
+                for b in bases:
+                    _lib.load().klnmf_ipc_close(ctypes.c_void_p(b))
+            except Exception:
+                pass
+
+    def _setup_peers(self) -> None:
+        """Map every other rank's factors and maintained-product arrays
+        (CUDA IPC; peer access over NVLink) for the fused exchange: the solver
+        kernels store each result into all copies as they produce it
+        (klnmf_solve_args_t.peer_*), and a half-step ends with a barrier
+        instead of an all-gather.  The values written are the ones the
+        all-gather would have moved, so results are bitwise those of the
+        all-gather path."""
+        import torch.distributed as dist
+
+        bufs = {"W": self.factors["W"], "F": self.factors["F"], "csc": self.t["csc"], "csr": self.t["csr"]}
+        mine = {}
+        for name, ten in bufs.items():
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_int64()
+            _lib.call("klnmf_ipc_export", ten.data_ptr(), h, ctypes.byref(off))
+            mine[name] = (bytes(h), off.value)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=self.group)
+        opened = {}  # one mapping per peer allocation, however many buffers it holds
+        peers = {}
+        for name in bufs:
+            ptrs = []
+            for q in range(self.world):
+                if q == self.rank_id:
+                    continue
+                hb, off = everyone[q][name]
+                if hb not in opened:
+                    base = ctypes.c_void_p()
+                    _lib.call("klnmf_ipc_open", hb, ctypes.byref(base))
+                    opened[hb] = base.value
+                ptrs.append(opened[hb] + off)
+            peers[name] = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+        self._ipc_bases = list(opened.values())
+        self._peers = peers
+        self._barrier_buf = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # every rank has mapped every peer before any kernel stores through a mapping
+        dist.barrier(group=self.group)
+
+    @property
+    def fused_exchange(self) -> bool:
+        return self._peers is not None
+
+    def _peer_barrier(self) -> None:
+        """Fused exchange: every rank's work enqueued so far is complete
+        before any rank's next work -- after a half-step, so its peer stores
+        have landed before anyone reads them; before one, so no peer still
+        reads (as the fixed factor, or for the objective) the values about to
+        be overwritten in its copy."""
+        import torch.distributed as dist
+
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._barrier_buf, group=self.group)  # stream-ordered
+        else:
+            torch.cuda.synchronize(self.dev)
+            dist.barrier(group=self.group)
 
     def _track(self, name, *tensors):
         if self.ledger is not None:
@@ -447,6 +522,8 @@ class DevicePlan:
             need = "csr" if which == "F" else "csc"
             if self.t_current != need:
                 self._init_t(need)
+        if self._peers is not None:
+            self._peer_barrier()
         key = (which, float(alpha), float(beta), tol, dev_sums, events is not None, self.concurrent)
         if self.use_graphs:
             entry = self._graphs.get(key)
@@ -544,6 +621,10 @@ class DevicePlan:
             a.tmap = side.tmap.data_ptr()
             a.t_in = self.t[need].data_ptr()
             a.t_out = self.t["csc" if which == "F" else "csr"].data_ptr()
+            if self._peers is not None:
+                a.n_peers = self.world - 1
+                a.peer_moving = self._peers[which].data_ptr()
+                a.peer_t = self._peers["csc" if which == "F" else "csr"].data_ptr()
         item_base = side.items.data_ptr()
         lib = _lib.load()
         main = self.stream_ptr
@@ -598,7 +679,12 @@ class DevicePlan:
 
     def _exchange(self, which: str) -> None:
         """All-gather the updated rows of the moving factor (and, in fp32
-        mode, the maintained products of the updated entries)."""
+        mode, the maintained products of the updated entries) -- or, with the
+        fused exchange, only wait until every rank's kernels have stored
+        theirs into all copies."""
+        if self._peers is not None:
+            self._peer_barrier()
+            return
         side = self.sides[which]
         allgather_ranges(self.factors[which], side.ranges, self.group)
         if self.fp32:

@@ -39,7 +39,7 @@ def test_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.Side) == 48
     # side, 12 pointers, r/rp, 5 doubles, inner_cap, stats, order mode/side, order seed, order_iter,
     # max_passes/reserved
-    assert ctypes.sizeof(_lib.SolveArgs) == 48 + 8 * 12 + 8 + 8 * 5 + 8 + 8 + 8 + 8 + 8 + 8
+    assert ctypes.sizeof(_lib.SolveArgs) == 48 + 8 * 12 + 8 + 8 * 5 + 8 + 8 + 8 + 8 + 8 + 8 + 16
 
 
 def test_errors_are_raised_loudly_without_a_device():

@@ -1,11 +1,13 @@
 """The sharded multi-rank path on the GPU: two ranks (processes) sharing one
 GPU over a gloo process group run factorize(shard=True) -- nnz-balanced
-subproblem ranges per rank, all-gather of the updated factor rows and
-maintained products after every half-step, stats all-reduced -- and must
-reproduce the single-process run BIT FOR BIT (the reference's worker
-invariance, pkg/tests/test_solver.py:162-173, across ranks).  The kernels of
-the two ranks never wait on each other: the exchange is a host-side
-collective between launches."""
+subproblem ranges per rank, the updated factor rows and maintained products
+exchanged after every half-step, stats all-reduced -- and must reproduce the
+single-process run BIT FOR BIT (the reference's worker invariance,
+pkg/tests/test_solver.py:162-173, across ranks).  Both exchanges are covered:
+the fused one (fp32 default: the kernels store their results into the peer's
+copies through CUDA-IPC mappings, then a barrier) and the all-gather.  The
+kernels of the two ranks never wait on each other: the synchronisation is a
+host-side collective between launches."""
 import os
 import pickle
 import socket
@@ -22,13 +24,23 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, precision, order, out):
+def _worker(rank, world, port, precision, order, fused, out):
+    os.environ["KLNMF_FUSED_EXCHANGE"] = "1" if fused else "0"
     import torch
     import torch.distributed as dist
 
     import paper_1604_04026_b200 as kb
+    from paper_1604_04026_b200 import plan as plan_mod
     from paper_1604_04026_b200 import synth
 
+    mapped = []
+    setup = plan_mod.DevicePlan._setup_peers
+
+    def recording_setup(self):
+        setup(self)
+        mapped.append(self.fused_exchange)
+
+    plan_mod.DevicePlan._setup_peers = recording_setup
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
@@ -42,23 +54,27 @@ def _worker(rank, world, port, precision, order, out):
             with open(out, "wb") as fh:
                 pickle.dump({"w": res.factors.w.values, "f": res.factors.f.values,
                              "total": [rec.total_objective for rec in res.log.records],
-                             "stats": (res.stats.cap_hits, res.stats.degenerate, res.stats.inner_iters)}, fh)
+                             "stats": (res.stats.cap_hits, res.stats.degenerate, res.stats.inner_iters),
+                             "fused": mapped}, fh)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("precision,order", [("fp32", "shared"), ("fp32", "counter"), ("fp64", "shared")])
-def test_two_ranks_match_one(cuda_ok, tmp_path, precision, order):
+@pytest.mark.parametrize("precision,order,fused", [("fp32", "shared", True), ("fp32", "counter", True),
+                                                   ("fp32", "shared", False), ("fp64", "shared", False)])
+def test_two_ranks_match_one(cuda_ok, tmp_path, precision, order, fused):
     import torch.multiprocessing as mp
 
     import paper_1604_04026_b200 as kb
     from paper_1604_04026_b200 import synth
 
     out = str(tmp_path / "rank0.pkl")
-    mp.start_processes(_worker, args=(2, _free_port(), precision, order, out), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, _free_port(), precision, order, fused, out), nprocs=2, join=True,
                        start_method="spawn")
     with open(out, "rb") as fh:
         two = pickle.load(fh)
+    # the fused exchange is the fp32 path's; fp64 and the opt-out all-gather
+    assert two["fused"] == ([True] if fused and precision == "fp32" else [])
     spec = synth.CONFIGS["C3"].scaled(m=4000)
     V = synth.generate(spec)
     w0, f0 = synth.initial_factors(spec, round_fp32=True)

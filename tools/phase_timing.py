@@ -55,12 +55,14 @@ torch.cuda.synchronize()
 assert fn(buf.ctypes.data, 0) == 0
 for kind, label in ((0, "cluster kernels"), (1, "cooperative kernel"), (2, "warp kernels (per warp)")):
     c = buf[kind].astype(np.float64)
-    tot = c[:8].sum()
+    tot = c[:8].sum() + c[12]
     if tot == 0:
         continue
     print(f"--- {label}: {tot / 1e9:.3f} G CTA-cycles over {timed} iteration(s)")
     for i, p in enumerate(PHASES):
         print(f"  {p:16s} {100 * c[i] / tot:5.1f}%")
+    if c[12]:
+        print(f"  {'first reduction':16s} {100 * c[12] / tot:5.1f}%  (per subproblem start, includes waiting for the group)")
     for i, p in enumerate(COUNTS):
         print(f"  {p:20s} {c[8 + i]:.0f}")
     per = lambda cyc, n: cyc / n if n else float("nan")  # noqa: E731
