@@ -284,28 +284,48 @@ class DevicePlan:
         import torch.distributed as dist
 
         bufs = {"W": self.factors["W"], "F": self.factors["F"], "csc": self.t["csc"], "csr": self.t["csr"]}
-        mine = {}
-        for name, ten in bufs.items():
-            h = (ctypes.c_char * 64)()
-            off = ctypes.c_int64()
-            _lib.call("klnmf_ipc_export", ten.data_ptr(), h, ctypes.byref(off))
-            mine[name] = (bytes(h), off.value)
+        mine, error = {}, None
+        try:
+            for name, ten in bufs.items():
+                h = (ctypes.c_char * 64)()
+                off = ctypes.c_int64()
+                _lib.call("klnmf_ipc_export", ten.data_ptr(), h, ctypes.byref(off))
+                mine[name] = (bytes(h), off.value)
+        except RuntimeError as exc:
+            error = str(exc)
         everyone = [None] * self.world
-        dist.all_gather_object(everyone, mine, group=self.group)
+        dist.all_gather_object(everyone, None if error else mine, group=self.group)
         opened = {}  # one mapping per peer allocation, however many buffers it holds
         peers = {}
-        for name in bufs:
-            ptrs = []
-            for q in range(self.world):
-                if q == self.rank_id:
-                    continue
-                hb, off = everyone[q][name]
-                if hb not in opened:
-                    base = ctypes.c_void_p()
-                    _lib.call("klnmf_ipc_open", hb, ctypes.byref(base))
-                    opened[hb] = base.value
-                ptrs.append(opened[hb] + off)
-            peers[name] = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+        if error is None and all(e is not None for e in everyone):
+            try:
+                for name in bufs:
+                    ptrs = []
+                    for q in range(self.world):
+                        if q == self.rank_id:
+                            continue
+                        hb, off = everyone[q][name]
+                        if hb not in opened:
+                            base = ctypes.c_void_p()
+                            _lib.call("klnmf_ipc_open", hb, ctypes.byref(base))
+                            opened[hb] = base.value
+                        ptrs.append(opened[hb] + off)
+                    peers[name] = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+            except RuntimeError as exc:
+                error = str(exc)
+        elif error is None:
+            error = "a peer rank could not export its buffers"
+        # all ranks take the same path: fused only if every rank mapped every peer
+        ok = [None] * self.world
+        dist.all_gather_object(ok, error is None, group=self.group)
+        if not all(ok):
+            for b in opened.values():
+                _lib.load().klnmf_ipc_close(ctypes.c_void_p(b))
+            import warnings
+
+            warnings.warn(f"fused peer exchange unavailable ({error or 'on another rank'}); "
+                          "falling back to the NCCL all-gather", RuntimeWarning)
+            return
         self._ipc_bases = list(opened.values())
         self._peers = peers
         self._barrier_buf = torch.zeros(1, dtype=torch.int32, device=self.dev)

@@ -25,7 +25,7 @@ def _free_port():
 
 
 def _worker(rank, world, port, precision, order, fused, out):
-    os.environ["KLNMF_FUSED_EXCHANGE"] = "1" if fused else "0"
+    os.environ["KLNMF_FUSED_EXCHANGE"] = "0" if fused is False else "1"
     import torch
     import torch.distributed as dist
 
@@ -41,6 +41,18 @@ def _worker(rank, world, port, precision, order, fused, out):
         mapped.append(self.fused_exchange)
 
     plan_mod.DevicePlan._setup_peers = recording_setup
+    if fused == "fail" and rank == 1:
+        # this rank cannot map its peer: every rank must fall back together
+        from paper_1604_04026_b200 import _lib
+
+        real_call = _lib.call
+
+        def failing_call(name, *args):
+            if name == "klnmf_ipc_open":
+                raise RuntimeError("klnmf_ipc_open failed (test)")
+            return real_call(name, *args)
+
+        _lib.call = failing_call
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
@@ -61,7 +73,8 @@ def _worker(rank, world, port, precision, order, fused, out):
 
 
 @pytest.mark.parametrize("precision,order,fused", [("fp32", "shared", True), ("fp32", "counter", True),
-                                                   ("fp32", "shared", False), ("fp64", "shared", False)])
+                                                   ("fp32", "shared", False), ("fp32", "shared", "fail"),
+                                                   ("fp64", "shared", False)])
 def test_two_ranks_match_one(cuda_ok, tmp_path, precision, order, fused):
     import torch.multiprocessing as mp
 
@@ -73,8 +86,10 @@ def test_two_ranks_match_one(cuda_ok, tmp_path, precision, order, fused):
                        start_method="spawn")
     with open(out, "rb") as fh:
         two = pickle.load(fh)
-    # the fused exchange is the fp32 path's; fp64 and the opt-out all-gather
-    assert two["fused"] == ([True] if fused and precision == "fp32" else [])
+    # the fused exchange is the fp32 path's; fp64 and the opt-out all-gather;
+    # a rank that cannot map its peer sends every rank to the all-gather
+    expect = {True: [True], False: [], "fail": [False]}[fused] if precision == "fp32" else []
+    assert two["fused"] == expect
     spec = synth.CONFIGS["C3"].scaled(m=4000)
     V = synth.generate(spec)
     w0, f0 = synth.initial_factors(spec, round_fp32=True)
