@@ -320,7 +320,10 @@ class DevicePlan:
         dist.all_gather_object(ok, error is None, group=self.group)
         if not all(ok):
             for b in opened.values():
-                _lib.load().klnmf_ipc_close(ctypes.c_void_p(b))
+                try:
+                    _lib.call("klnmf_ipc_close", ctypes.c_void_p(b))
+                except RuntimeError:
+                    pass
             import warnings
 
             warnings.warn(f"fused peer exchange unavailable ({error or 'on another rank'}); "
