@@ -26,6 +26,7 @@ cpu_baseline  the reference algorithm (oracle port of _kernels.sweep_range, dens
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -430,7 +431,11 @@ def run_ours(args):
             "clocks": clocks.summary(),
         }
 
-    # e2e: public API from host buffers, rank-local
+    # e2e: public API from host buffers, rank-local (a fresh call: the
+    # device-timed plan above is released first)
+    del plan
+    gc.collect()
+    torch.cuda.empty_cache()
     if not args.no_e2e and not args.profile:
         cfg = NmfConfig(rank=r, reg=reg, max_outer_iters=args.steps, rel_obj_tol=0.0, seed=spec.seed,
                         log_objectives=False, precision=precision, device=local, shard=world > 1)

@@ -598,10 +598,17 @@ class DevicePlan:
         evs: list = []
         saved = self.stream_ptr
         try:
-            with torch.cuda.graph(graph, stream=capture_stream):
-                self.stream_ptr = capture_stream.cuda_stream
-                self._capturing = True
-                self._launch(which, alpha, beta, tol, dev_sums, evs if with_events else None)
+            # capture_begin/end rather than torch.cuda.graph(): the context
+            # manager also runs gc.collect() and empty_cache(), which hands
+            # every cached block (GBs of plan buffers) back to the driver
+            with torch.cuda.stream(capture_stream):
+                graph.capture_begin()
+                try:
+                    self.stream_ptr = capture_stream.cuda_stream
+                    self._capturing = True
+                    self._launch(which, alpha, beta, tol, dev_sums, evs if with_events else None)
+                finally:
+                    graph.capture_end()
         except Exception:  # capture unsupported here: stay eager
             self.use_graphs = False
             return None
