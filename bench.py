@@ -434,7 +434,9 @@ def run_ours(args):
     # e2e: public API from host buffers, rank-local (a fresh call: the
     # device-timed plan above is released first)
     del plan
-    gc.collect()
+    gc.collect()  # closes this rank's peer mappings (fused exchange)
+    if world > 1:
+        dist.barrier()  # ... on every rank before any rank releases the memory
     torch.cuda.empty_cache()
     if not args.no_e2e and not args.profile:
         cfg = NmfConfig(rank=r, reg=reg, max_outer_iters=args.steps, rel_obj_tol=0.0, seed=spec.seed,
