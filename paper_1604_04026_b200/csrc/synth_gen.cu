@@ -104,9 +104,10 @@ __global__ void phi_cdf_kernel(Rng rng, int64_t n, double zipf, double zipf_norm
         if (threadIdx.x == 0) carry = c0 + total;
         __syncthreads();
     }
+    // normalise; the last entry is pinned to exactly 1 by the thread that owns
+    // it (a separate store from another thread would race with this one)
     const double tot = carry;
-    for (int64_t i = threadIdx.x; i < n; i += NT) row[i] = row[i] / tot;
-    if (threadIdx.x == 0) row[n - 1] = 1.0;
+    for (int64_t i = threadIdx.x; i < n; i += NT) row[i] = i == n - 1 ? 1.0 : row[i] / tot;
 }
 
 __global__ void lengths_kernel(Rng rng, int64_t m, int kind, double mean, double sigma, int64_t *len) {
