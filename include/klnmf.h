@@ -235,6 +235,11 @@ int klnmf_layout_to_device(const double *src, int64_t r, int64_t n, const int32_
                            int32_t rp, void *dst, int fp32, void *stream);
 int klnmf_layout_from_device(const void *src, int64_t r, int64_t n, const int32_t *order,
                              int32_t rp, int fp32, double *dst, void *stream);
+/* fp32 factor (item-major, visit order) -> (r, n) natural-order fp32: the
+ * values an fp32-mode download widens exactly on the host
+ * (klnmf_download_f32_as_f64), half the bytes of the fp64 layout. */
+int klnmf_layout_from_device_f32(const float *src, int64_t r, int64_t n, const int32_t *order, int32_t rp,
+                                 float *dst, void *stream);
 
 /* CSC (ptr/idx/val) -> CSC of the transpose, plus both entry maps:
  * map_t2o[q'] = position in the input of output entry q', map_o2t = inverse.

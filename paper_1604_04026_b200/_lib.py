@@ -53,6 +53,7 @@ EXPORTS = (
     "klnmf_row_sums_fast",
     "klnmf_layout_to_device",
     "klnmf_layout_from_device",
+    "klnmf_layout_from_device_f32",
     "klnmf_transpose",
     "klnmf_coo_to_csc",
     "klnmf_bucketize",
@@ -158,6 +159,7 @@ _SIGS = {
     "klnmf_row_sums_fast": ([P, I64, I32, I32, P, P], INT),
     "klnmf_layout_to_device": ([P, I64, I64, P, I32, P, INT, P], INT),
     "klnmf_layout_from_device": ([P, I64, I64, P, I32, INT, P, P], INT),
+    "klnmf_layout_from_device_f32": ([P, I64, I64, P, I32, P, P], INT),
     "klnmf_transpose": ([P, P, P, INT, I64, I64, I64, P, P, P, P, P, P], INT),
     "klnmf_coo_to_csc": ([P, P, P, INT, I64, I64, I64, P, P, P, P, P], INT),
     "klnmf_bucketize": ([P, I64, I64, P, INT, P, P, P], INT),

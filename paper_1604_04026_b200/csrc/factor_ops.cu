@@ -27,15 +27,15 @@ __global__ void to_device_kernel(const double *src, int64_t r, int64_t n, const 
     }
 }
 
-template <typename T>
+template <typename T, typename D>
 __global__ void from_device_kernel(const T *src, int64_t r, int64_t n, const int32_t *order,
-                                   int32_t rp, double *dst) {
+                                   int32_t rp, D *dst) {
     const int64_t total = n * r;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / r;
         const int tt = (int)(e - i * r);
-        dst[(int64_t)order[tt] * n + i] = (double)src[i * rp + tt];
+        dst[(int64_t)order[tt] * n + i] = (D)src[i * rp + tt];
     }
 }
 
@@ -156,11 +156,20 @@ extern "C" int klnmf_layout_from_device(const void *src, int64_t r, int64_t n, c
     const int64_t total = n * r;
     if (total == 0) return 0;
     if (fp32)
-        from_device_kernel<float><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+        from_device_kernel<float, double><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
             static_cast<const float *>(src), r, n, order, rp, dst);
     else
-        from_device_kernel<double><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+        from_device_kernel<double, double><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
             static_cast<const double *>(src), r, n, order, rp, dst);
+    KLNMF_CHECK_LAUNCH("from_device_kernel");
+    return 0;
+}
+
+extern "C" int klnmf_layout_from_device_f32(const float *src, int64_t r, int64_t n, const int32_t *order,
+                                            int32_t rp, float *dst, void *stream) {
+    const int64_t total = n * r;
+    if (total == 0) return 0;
+    from_device_kernel<float, float><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, r, n, order, rp, dst);
     KLNMF_CHECK_LAUNCH("from_device_kernel");
     return 0;
 }

@@ -450,12 +450,19 @@ class DevicePlan:
         """Download both factors as (r, n) / (r, m) fp64 numpy arrays."""
         out = []
         for name, n_items in (("W", self.n), ("F", self.m)):
-            dst = torch.empty(self.r, n_items, dtype=torch.float64, device=self.dev)
             o = torch.from_numpy(self._padded(self.order[name])).to(self.dev)
-            _lib.call("klnmf_layout_from_device", self.factors[name].data_ptr(), self.r, n_items, o.data_ptr(),
-                      self.rp, int(self.fp32), dst.data_ptr(), self.stream_ptr)
             host = np.empty((self.r, n_items), dtype=np.float64)
-            _lib.call("klnmf_download_f64", dst.data_ptr(), host.size, host.ctypes.data, self.stream_ptr)
+            if self.fp32:
+                # fp32 values cross PCIe and are widened (exactly) on host threads
+                dst = torch.empty(self.r, n_items, dtype=torch.float32, device=self.dev)
+                _lib.call("klnmf_layout_from_device_f32", self.factors[name].data_ptr(), self.r, n_items,
+                          o.data_ptr(), self.rp, dst.data_ptr(), self.stream_ptr)
+                _lib.call("klnmf_download_f32_as_f64", dst.data_ptr(), host.size, host.ctypes.data, self.stream_ptr)
+            else:
+                dst = torch.empty(self.r, n_items, dtype=torch.float64, device=self.dev)
+                _lib.call("klnmf_layout_from_device", self.factors[name].data_ptr(), self.r, n_items, o.data_ptr(),
+                          self.rp, 0, dst.data_ptr(), self.stream_ptr)
+                _lib.call("klnmf_download_f64", dst.data_ptr(), host.size, host.ctypes.data, self.stream_ptr)
             out.append(host)
         return out[0], out[1]
 
