@@ -308,13 +308,13 @@ __device__ __forceinline__ void flush_stats(const Counters &cnt, bool lead, unsi
 // Diagnostic build only (build.py variant "phase", tools/phase_timing.py):
 // clock cycles per phase of the long-row kernels, thread 0 of every CTA,
 // [kind][slot], kind 0 = cluster, 1 = cooperative, 2 = warp kernels (lane 0
-// of every warp).  Slots 0-7 are cycles
+// of every warp), 3 = block kernels (thread 0).  Slots 0-7 are cycles
 // (init, gather, pass, chunk reduction, scalar Newton, update/re-evaluation,
 // re-evaluation reduction, final writes), 8-11 counts (chunk reductions,
 // re-evaluation reductions, moves, chunks), 12 the cycles of each subproblem's
 // first reduction (which also waits for the slowest CTA of the group to arrive).
 #ifdef KLNMF_PHASE_TIMING
-__device__ unsigned long long g_phase[3][16];
+__device__ unsigned long long g_phase[4][16];
 __device__ __forceinline__ long long phase_now() {
     long long n;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(n));
@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     const int tid = threadIdx.x;
     const int64_t slot = blockIdx.x;
     if (slot >= a.n_items) return;
+    PhaseClock ph;
     const Params pm(a);
     const int rp = a.rp, r = a.r;
     const float *fixed = static_cast<const float *>(a.fixed);
@@ -612,12 +613,15 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) issue(st);
     __syncthreads();
+    ph.mark(0);
 
     Counters cnt;
     int buf = 0, cur = 0;  // cur: buffer holding the last pass's sums
     for (int ch = 0; ch < nchunks; ++ch) {
+        ph.count(11);
         issue(ch + STAGES - 1);
         cp_wait<STAGES - 1>();
+        ph.mark(1);
         const float4 *Ach = ring + (ch % STAGES) * NPL * NT + tid;
         const int pc = phys(ch);
         const int nc = min(C, r - pc * C);
@@ -634,7 +638,10 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                     for (int e = 0; e < NPL; ++e)
                         accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], entry_z(u[e], vi[e]));
                 });
+                ph.mark(2);
                 bs.reduce(red, buf);
+                ph.mark(3);
+                ph.count(8);
                 cur = buf;
                 buf ^= 1;
                 fresh = true;
@@ -649,7 +656,9 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
             while (active) {  // block-uniform
                 bool again = false;
                 const double delta = newton_step(g, h, x, inner, active, again, pm, cnt);
+                ph.mark(4);
                 if (delta != 0.0) {
+                    ph.count(10);
                     moved = true;
                     with_clamp(delta < 0.0, [&](auto cl) {
 #pragma unroll
@@ -658,12 +667,15 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                                                               vi[e]);
                     });
                 }
+                ph.mark(5);
                 if (again) {
                     double g2 = 0.0, h2 = 0.0;
 #pragma unroll
                     for (int e = 0; e < NPL; ++e)
                         accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, cc)));
                     bs.reduce2(g2, h2, buf);
+                    ph.mark(6);
+                    ph.count(9);
                     g = (base + pm.alpha * x) - bs.get(buf, 0);
                     h = pm.alpha + bs.get(buf, 1);
                     buf ^= 1;
@@ -673,6 +685,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
             }
             if (moved) fresh = false;
             if (tid == 0) xo[tt] = (float)x;
+            ph.mark(4);
         }
     }
     cp_wait<0>();
@@ -682,6 +695,8 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     for (int e = 0; e < NPL; ++e)
         if (tid + e * NT < s) put_t(a, lo + tid + e * NT, entry_t(u[e], vi[e], pm.eps_div));
     flush_stats(cnt, tid == 0, a.stats, false);
+    ph.mark(7);
+    ph.flush(3, tid == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1194,7 +1209,7 @@ inline size_t slice_smem(int rp) {
 extern "C" int klnmf_debug_phase(unsigned long long *out, int reset) {
     if (cudaMemcpyFromSymbol(out, klnmf::g_phase, sizeof(klnmf::g_phase)) != cudaSuccess) return 1;
     if (reset) {
-        static const unsigned long long zero[3][16] = {};
+        static const unsigned long long zero[4][16] = {};
         if (cudaMemcpyToSymbol(klnmf::g_phase, zero, sizeof(zero)) != cudaSuccess) return 1;
     }
     return 0;

@@ -4,8 +4,8 @@ on steady-state iterations, from the diagnostic build
 
     python tools/phase_timing.py [cfg] [warm_iters] [timed_iters]
 
-Thread 0 of every cluster / cooperative CTA and lane 0 of every warp-kernel
-warp accumulate the cycles between phase marks; the table gives each phase's
+Thread 0 of every cluster / cooperative / block-kernel CTA and lane 0 of
+every warp-kernel warp accumulate the cycles between phase marks; the table gives each phase's
 share of that time and its mean per event (cycles per chunk reduction, per
 re-evaluation reduction, per move).
 """
@@ -36,7 +36,7 @@ w0, f0 = synth.initial_factors(spec)
 lib = _lib.load()
 fn = lib.klnmf_debug_phase
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros((3, 16), dtype=np.uint64)
+buf = np.zeros((4, 16), dtype=np.uint64)
 
 plan = DevicePlan(V, spec.rank, spec.precision)
 rng = np.random.default_rng(spec.seed)
@@ -53,7 +53,8 @@ for it in range(1, warm + timed + 1):
     ids = nxt
 torch.cuda.synchronize()
 assert fn(buf.ctypes.data, 0) == 0
-for kind, label in ((0, "cluster kernels"), (1, "cooperative kernel"), (2, "warp kernels (per warp)")):
+for kind, label in ((0, "cluster kernels"), (1, "cooperative kernel"), (2, "warp kernels (per warp)"),
+                    (3, "block kernels (per block)")):
     c = buf[kind].astype(np.float64)
     tot = c[:8].sum() + c[12]
     if tot == 0:
