@@ -1293,6 +1293,9 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
     if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
         return set_error_msg(1, "klnmf_solve_fast: bad coordinate order mode");
     if (!(args->eps_div > 0.0)) return set_error_msg(1, "klnmf_solve_fast: the fp32 mode needs eps_div > 0");
+    // the gather offsets of the fixed factor are 32-bit (register budget)
+    if (args->side.n_fix * (int64_t)args->rp >= (int64_t)INT32_MAX)
+        return set_error_msg(1, "klnmf_solve_fast: fixed-factor items x padded rank must be < 2^31 in the fp32 mode");
     if (args->n_peers < 0 || (args->n_peers > 0 && (!args->peer_moving || !args->peer_t)))
         return set_error_msg(1, "klnmf_solve_fast: n_peers > 0 needs both peer pointer arrays");
     const FastKernel &k = kFast[kernel_id];
@@ -1352,6 +1355,9 @@ extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *sche
     if (args->order_mode != KLNMF_ORDER_SHARED && (args->order_mode != KLNMF_ORDER_COUNTER || !args->order_iter))
         return set_error_msg(1, "klnmf_solve_coop: bad coordinate order mode");
     if (!(args->eps_div > 0.0)) return set_error_msg(1, "klnmf_solve_coop: the fp32 mode needs eps_div > 0");
+    // the gather offsets of the fixed factor are 32-bit (register budget)
+    if (args->side.n_fix * (int64_t)args->rp >= (int64_t)INT32_MAX)
+        return set_error_msg(1, "klnmf_solve_coop: fixed-factor items x padded rank must be < 2^31 in the fp32 mode");
     if (args->n_peers < 0 || (args->n_peers > 0 && (!args->peer_moving || !args->peer_t)))
         return set_error_msg(1, "klnmf_solve_coop: n_peers > 0 needs both peer pointer arrays");
     cudaStream_t st = as_stream(stream);

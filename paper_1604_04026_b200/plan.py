@@ -118,6 +118,9 @@ class DevicePlan:
             raise ValueError("the counter coordinate order is an fp32-mode option (fp64 is the oracle mode)")
         if precision == "fp32" and round_rp(int(rank)) > 256:
             raise ValueError("the fp32 mode supports rank <= 256 (use precision='fp64' above that)")
+        if precision == "fp32" and max(int(V.shape[0]), int(V.shape[1])) * round_rp(int(rank)) >= 2**31 - 1:
+            raise ValueError("the fp32 mode needs max(n, m) x padded rank < 2^31 (32-bit gather offsets); "
+                             "use precision='fp64' or a smaller rank")
         self.order_mode = _lib.ORDER_COUNTER if order == "counter" else _lib.ORDER_SHARED
         self.order_seed = int(order_seed) & (2**64 - 1)
         if not torch.cuda.is_available():

@@ -119,3 +119,17 @@ def test_synth_configs_shapes():
     assert np.all(V.values >= 1.0) and np.all(V.values == np.round(V.values))
     V2 = synth.generate(spec)
     assert np.array_equal(V.row_idx, V2.row_idx)
+
+
+def test_fp32_plan_rejects_32bit_offset_overflow():
+    # fp32 kernels address the fixed factor with 32-bit offsets: a shape whose
+    # items x padded rank reaches 2^31 must be refused loudly, not wrap
+    import types
+
+    import pytest
+
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    huge = types.SimpleNamespace(shape=(30_000_000, 10))
+    with pytest.raises(ValueError, match="2\\^31"):
+        DevicePlan(huge, 100, "fp32")
