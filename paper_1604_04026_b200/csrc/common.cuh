@@ -26,6 +26,25 @@ int set_error_msg(int code, const char *msg);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Scratch of the plan-building helpers comes from the device's default
+// stream-ordered pool (cudaMallocAsync).  Its default release threshold of 0
+// hands freed memory back to the driver at every synchronisation, so the next
+// plan re-maps GBs (seen as 0.05-0.5 s stalls of a C4 transpose); keep it in
+// the pool instead (once per device; the scratch stays reserved in-process).
+inline cudaError_t keep_async_pool() {
+    static bool kept[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess || dev < 0 || dev >= 64 || kept[dev]) return e;
+    cudaMemPool_t pool;
+    e = cudaDeviceGetDefaultMemPool(&pool, dev);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e == cudaSuccess) kept[dev] = true;
+    return e;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size,
 // so launch paths replayed under CUDA-graph capture issue no attribute calls.
 cudaError_t ensure_smem(const void *fn, size_t bytes);

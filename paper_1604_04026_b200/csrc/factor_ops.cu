@@ -178,6 +178,7 @@ extern "C" int klnmf_row_sums_fast(const float *fac, int64_t n_items, int32_t rp
                                    double *out, void *stream) {
     cudaStream_t st = as_stream(stream);
     double *partial = nullptr;
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (size_t)RS_BLOCKS * (size_t)rp, st));
     const int nt = rp < 128 ? ((rp + 31) / 32) * 32 : 128;
     row_sums_fast_partial<<<RS_BLOCKS, nt, 0, st>>>(fac, n_items, rp, partial);
@@ -193,6 +194,7 @@ extern "C" int klnmf_factor_stats(const void *fac, int64_t n_items, int32_t rp, 
     cudaStream_t st = as_stream(stream);
     constexpr int NT = 256, NB = 512;
     double *partial = nullptr;
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (NB * 3 + 3), st));
     if (fp32)
         factor_stats_partial<float, NT><<<NB, NT, 0, st>>>(static_cast<const float *>(fac), n_items, rp, r, partial);
@@ -235,6 +237,7 @@ extern "C" int klnmf_kl_data_term_t(const float *val, const double *t, int64_t n
                                     double *out_host, void *stream) {
     cudaStream_t st = as_stream(stream);
     double *partial = nullptr;
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (KL_BLOCKS + 1), st));
     kl_t_partial<<<KL_BLOCKS, KL_NT, 0, st>>>(val, t, nnz, eps_div, partial);
     KLNMF_CHECK_LAUNCH("kl_t_partial");

@@ -431,6 +431,7 @@ extern "C" int klnmf_kl_data_term_dev(const klnmf_side_t *csc, const void *w, co
     const int64_t nnz = csc->nnz;
     const int64_t blocks = nnz > 0 ? (nnz + NT - 1) / NT : 1;
     double *partial = nullptr;
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (size_t)(blocks + 1), st));
     if (nnz > 0) {
         if (fp32)

@@ -117,6 +117,7 @@ template <typename V>
 int transpose_impl(const int64_t *ptr, const int32_t *idx, const V *val, int64_t n_rows, int64_t n_cols,
                    int64_t nnz, int64_t *ptr_t, int32_t *idx_t, V *val_t, int32_t *map_t2o, int32_t *map_o2t,
                    cudaStream_t st) {
+    KLNMF_CHECK(keep_async_pool());
     if (nnz == 0) {
         KLNMF_CHECK(cudaMemsetAsync(ptr_t, 0, sizeof(int64_t) * (size_t)(n_rows + 1), st));
         return 0;
@@ -149,6 +150,7 @@ int transpose_impl(const int64_t *ptr, const int32_t *idx, const V *val, int64_t
 template <typename V>
 int coo_impl(const int32_t *rows, const int32_t *cols, const V *vals, int64_t nnz, int64_t n_rows, int64_t n_cols,
              int64_t *ptr, int32_t *idx, V *val, int32_t *dup_flag, cudaStream_t st) {
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMemsetAsync(dup_flag, 0, sizeof(int32_t), st));
     if (nnz == 0) {
         KLNMF_CHECK(cudaMemsetAsync(ptr, 0, sizeof(int64_t) * (size_t)(n_cols + 1), st));
@@ -229,6 +231,7 @@ extern "C" int klnmf_bucketize(const int64_t *ptr, int64_t j_lo, int64_t j_hi, c
     }
     int64_t *sizes = nullptr, *sizes_sorted = nullptr, *dbounds = nullptr, *dcounts = nullptr;
     int32_t *ids = nullptr;
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&sizes, sizeof(int64_t) * (size_t)n, st));
     KLNMF_CHECK(cudaMallocAsync(&sizes_sorted, sizeof(int64_t) * (size_t)n, st));
     KLNMF_CHECK(cudaMallocAsync(&ids, sizeof(int32_t) * (size_t)n, st));

@@ -238,6 +238,7 @@ extern "C" int klnmf_synth_build(uint64_t seed, int64_t n, int64_t m, int32_t to
         for (int64_t i = 1; i <= n; ++i) zipf_norm += pow((double)i, -zipf);
     double *phi = nullptr;
     int64_t *len = nullptr, *off = nullptr;
+    KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&phi, sizeof(double) * (size_t)topics * (size_t)n, st));
     KLNMF_CHECK(cudaMallocAsync(&len, sizeof(int64_t) * (size_t)m, st));
     KLNMF_CHECK(cudaMallocAsync(&off, sizeof(int64_t) * (size_t)(m + 1), st));
