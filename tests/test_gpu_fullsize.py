@@ -17,7 +17,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(name, iters):
+def _run(name, iters, order="shared"):
     import torch
 
     from paper_1604_04026_b200 import synth
@@ -25,7 +25,7 @@ def _run(name, iters):
 
     spec = synth.CONFIGS[name]
     V = synth.generate_device(spec)
-    plan = DevicePlan(V, spec.rank, spec.precision)
+    plan = DevicePlan(V, spec.rank, spec.precision, order=order, order_seed=spec.seed)
     del V
     r = spec.rank
     g = torch.Generator(device="cuda").manual_seed(spec.seed)
@@ -54,12 +54,12 @@ def _run(name, iters):
     return out
 
 
-@pytest.mark.parametrize("name,iters", [("C4", 4), ("C5", 3)])
-def test_full_size_deterministic_and_descending(cuda_ok, name, iters):
+@pytest.mark.parametrize("name,iters,order", [("C4", 4, "shared"), ("C4", 4, "counter"), ("C5", 3, "shared")])
+def test_full_size_deterministic_and_descending(cuda_ok, name, iters, order):
     import torch
 
-    a = _run(name, iters)
-    b = _run(name, iters)
+    a = _run(name, iters, order)
+    b = _run(name, iters, order)
     assert a["nnz"] == b["nnz"]
     assert torch.equal(a["W"], b["W"]) and torch.equal(a["F"], b["F"])
     assert torch.equal(a["t"], b["t"])
