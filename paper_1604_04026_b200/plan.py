@@ -18,11 +18,13 @@ Precision modes:
 
 Multi-GPU (torch.distributed, one process per GPU): every rank holds V and
 both factors in full; subproblems are split into contiguous nnz-balanced
-ranges (columns for the F-update, rows for the W-update); after each
-half-step the updated factor rows (and, in fp32 mode, the maintained
-products of the updated entries) are all-gathered.  Results are bitwise
-independent of the rank count: each subproblem is solved by exactly one rank
-with identical inputs, and row sums are computed from the full replica.
+ranges (columns for the F-update, rows for the W-update).  In fp32 mode the
+solver kernels store every result into all ranks' copies through CUDA-IPC
+mappings (the fused exchange, a barrier before and after each half-step);
+otherwise, after each half-step, the updated factor rows are all-gathered
+over NCCL.  Results are bitwise independent of the rank count: each
+subproblem is solved by exactly one rank with identical inputs, and row sums
+are computed from the full replica.
 
 torch is used here only as plumbing: device allocation, the current stream,
 and NCCL collectives.  All arithmetic runs in libklnmf.so.
@@ -31,12 +33,15 @@ and NCCL collectives.  All arithmetic runs in libklnmf.so.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import os
 import time
-import dataclasses
 
 import numpy as np
 import torch
+
+from . import _lib
+from .subproblem import SolveStats, Tolerances
 
 _TIMING = bool(os.environ.get("KLNMF_TIMING"))
 
@@ -54,10 +59,7 @@ class _Ticker:
             now = time.perf_counter()
             print(f"[klnmf] {self.what}: {label} {1e3 * (now - self.t):.1f} ms", flush=True)
             self.t = now
-_COOP_PARALLEL = bool(os.environ.get("KLNMF_COOP_PARALLEL"))
 
-from . import _lib
-from .subproblem import SolveStats, Tolerances
 
 INT64_MAX = np.iinfo(np.int64).max
 
@@ -674,7 +676,7 @@ class DevicePlan:
         # the other buckets are independent (disjoint outputs, atomic stats)
         # and fork over several streams, so one bucket's last partial wave and
         # the few-subproblem buckets overlap the others
-        first = [b for b in buckets if self.fp32 and b[0] == coop_kid and not _COOP_PARALLEL]
+        first = [b for b in buckets if self.fp32 and b[0] == coop_kid]
         rest = [b for b in buckets if b not in first]
         n_par = min(len(self._par_streams), len(rest)) if (self.fp32 and self.concurrent) else 0
         for q, (kid, start, count) in enumerate(first + rest):
