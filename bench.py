@@ -1,7 +1,11 @@
 #!/usr/bin/env python
 """Benchmark of the SRCD hot path (one outer iteration = F half-step + W half-step).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C5] [--impl ours|reference]
+
+With --gpus N > 1 and no torchrun environment, the script re-launches itself
+through ``torch.distributed.run --nproc-per-node N`` (one process per GPU,
+NCCL; it fails if fewer than N GPUs are visible).
 
 Default workload: BASELINE.json config C4 (102,660 x 300,000, ~68M nnz,
 r=100, alpha1=alpha2=0.01, fp32 storage / fp64 arithmetic) -- the config the
@@ -20,7 +24,12 @@ roofline   the dominant solver kernel: SURVEY.md §8(d) algorithmic bytes of the
            launch / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline  the reference algorithm (oracle port of _kernels.sweep_range, dense
            maintained product as in the reference) on the host cores, on a
-           stratified sample of subproblems, extrapolated to a full iteration.
+           stratified sample of subproblems, extrapolated to a full iteration,
+           AT THE STATE OF THE TIMED WINDOW: the factors and visit order the
+           GPU holds after its warm-up (iteration W+1).  The reference arm
+           (--impl reference) reaches the same iteration by running W full
+           iterations of the reference algorithm (oracle, support-t variant:
+           bitwise the reference's iterates) before its sampled steps.
 """
 
 from __future__ import annotations
@@ -54,12 +63,44 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU-baseline sample budget")
+    ap.add_argument("--cpu-seconds", type=float, default=6.0,
+                    help="wall seconds of one CPU-baseline sample (both arms use the same budget per sample)")
+    ap.add_argument("--cpu-samples", type=int, default=3, help="CPU-baseline samples of the GPU arm")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-kernel-events", action="store_true")
+    ap.add_argument("--e2e-jobs", type=int, default=None, help="complete factorize jobs timed for e2e "
+                    "(default 5; 1 for C5)")
     return ap.parse_args()
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks of this script, one per
+    GPU, through torch.distributed.run (rendezvous on 127.0.0.1)."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if args.gpus > have:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} CUDA device(s) are visible"}),
+              flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # the communicator lines (ranks, transports, NVLS) go to stderr
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(launch_cmd(args.gpus, port, sys.argv[1:]), env=env)
+
+
+def launch_cmd(gpus: int, port: int, argv) -> list:
+    """The torchrun command of a --gpus N run: N ranks of this script on one node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
 
 
 def peaks():
@@ -143,67 +184,71 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------
-def cpu_reference_sample(V, w0, f0, spec, seconds: float, threads: int):
-    """Time the reference algorithm (oracle port of _kernels.sweep_range with
-    the reference's dense length-n maintained product) on a stratified sample
-    of subproblems per nnz bucket and side, using `threads` host threads;
-    extrapolate to one outer iteration.  Returns (updates/s, sample text)."""
+SAMPLE_EDGES = [0, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 16384, 65536, 1 << 62]
+
+
+def cpu_reference_sample(V, w, f, spec, ids, seconds: float, threads: int, pick_seed: int = 123, vt=None):
+    """Time the reference algorithm on the host cores at a given state.
+
+    The reference's own per-column code path (oracle port of
+    _kernels.sweep_range, _kernels.py:123-144, with its dense length-N_fix
+    maintained product) solves a stratified sample of subproblems of both
+    sides at the state (w, f, ids) -- the factors and visit order of the
+    iteration being timed.  Every sampled column's thread CPU time is
+    recorded; the side's serial cost is sum_b mean_b * |bucket b|, and the
+    iteration time is the serial cost / threads (ideal parallel scaling over
+    the host cores, which flatters the reference).  Returns (updates/s,
+    seconds per iteration, subproblems sampled, Newton steps per visit)."""
     import oracle
 
     oracle.build()
     r = spec.rank
     reg = spec.reg
-    pt, rt, vt, _ = oracle.transpose_csc(V.n_rows, V.n_cols, V.col_ptr, V.row_idx, V.values)
-    sides = [("F", V.col_ptr, V.row_idx, V.values, w0, f0, reg.alpha2, reg.beta2),
-             ("W", pt, rt, vt, f0, w0, reg.alpha1, reg.beta1)]
-    ids = np.random.default_rng(spec.seed).permutation(r)
-    edges = [0, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 1 << 62]
-    rng = np.random.default_rng(123)
-    total_time = 0.0
+    if vt is None:
+        vt = oracle.transpose_csc(V.n_rows, V.n_cols, V.col_ptr, V.row_idx, V.values)[:3]
+    pt, rt, vtv = vt
+    sides = [("F", V.col_ptr, V.row_idx, V.values, w, f, reg.alpha2, reg.beta2),
+             ("W", pt, rt, vtv, f, w, reg.alpha1, reg.beta1)]
+    rng = np.random.default_rng(pick_seed)
+    total_cpu = 0.0
     sampled = 0
-    per_side_budget = seconds / 2
+    newton = 0
+    per_side = seconds * threads / 2.0  # thread-seconds of sampling per side
     for name, ptr, idx, val, fixed, moving, a, b in sides:
         sizes = np.diff(ptr)
         sums = oracle.row_sums(fixed)
-        buckets = [np.nonzero((sizes > lo) & (sizes <= hi))[0] for lo, hi in zip(edges[:-1], edges[1:])]
-        buckets = [np.nonzero(sizes == 0)[0]] + buckets
-        # calibrate: one column of the median bucket
-        est = []
-        for members in buckets:
-            if len(members) == 0:
-                est.append(0.0)
-                continue
-            j = int(members[len(members) // 2])
-            t0 = time.perf_counter()
-            _run_cols(oracle, ptr, idx, val, fixed, sums, moving, [j], ids, a, b, 1)
-            est.append(time.perf_counter() - t0)
-        side_time = 0.0
-        for members, e in zip(buckets, est):
-            if len(members) == 0:
-                continue
-            # sample count: all members of small buckets, else what fits the budget share
-            share = per_side_budget / max(1, sum(1 for q in buckets if len(q)))
-            k = int(min(len(members), max(threads, share * threads / max(e, 1e-6))))
-            pick = np.sort(rng.choice(members, size=k, replace=False))
-            t0 = time.perf_counter()
-            _run_cols(oracle, ptr, idx, val, fixed, sums, moving, pick, ids, a, b, threads)
-            dt = time.perf_counter() - t0
-            side_time += dt * len(members) / k
-            sampled += k
-        total_time += side_time
-    updates = 2.0 * V.nnz * r
-    return updates / total_time, total_time, sampled
-
-
-def _run_cols(oracle, ptr, idx, val, fixed, sums, moving, cols, ids, a, b, threads):
-    """sweep_range over an explicit column subset (sub-CSC), threads over columns."""
-    cols = np.asarray(cols, dtype=np.int64)
-    sizes = ptr[cols + 1] - ptr[cols]
-    sub_ptr = np.zeros(len(cols) + 1, dtype=np.int64)
-    np.cumsum(sizes, out=sub_ptr[1:])
-    sel = np.concatenate([np.arange(ptr[j], ptr[j + 1]) for j in cols]) if len(cols) else np.zeros(0, np.int64)
-    mov = np.ascontiguousarray(moving[:, cols])
-    oracle.sweep(sub_ptr, idx[sel], val[sel], fixed, sums, mov, ids, a, b, n_workers=threads, variant="dense")
+        buckets = [np.nonzero((sizes > lo) & (sizes <= hi))[0] for lo, hi in zip(SAMPLE_EDGES[:-1], SAMPLE_EDGES[1:])]
+        buckets = [q for q in [np.nonzero(sizes == 0)[0]] + buckets if len(q)]
+        mov = np.ascontiguousarray(moving).copy()  # sampled columns are solved in place
+        # calibration: a few members of every bucket (all in one threaded call)
+        calib = [np.sort(rng.choice(q, size=min(len(q), 4), replace=False)) for q in buckets]
+        st, secs = oracle.sweep_cols_timed(ptr, idx, val, fixed, sums, mov, np.concatenate(calib), ids, a, b,
+                                           n_workers=threads)
+        est, pos = [], 0
+        for c in calib:
+            est.append(max(float(np.mean(secs[pos:pos + len(c)])), 1e-7))
+            pos += len(c)
+        # allocation: every bucket gets an equal share of the thread-seconds
+        share = per_side / len(buckets)
+        picks = []
+        for q, c, e in zip(buckets, calib, est):
+            rest = np.setdiff1d(q, c, assume_unique=True)
+            k = int(min(len(rest), max(0, share / e - len(c))))
+            picks.append(np.sort(rng.choice(rest, size=k, replace=False)) if k > 0 else rest[:0])
+        cols = np.concatenate(picks) if picks else np.zeros(0, np.int64)
+        # longest first so no thread finishes last with a long column
+        cols = cols[np.argsort(-sizes[cols], kind="stable")]
+        st2, secs2 = oracle.sweep_cols_timed(ptr, idx, val, fixed, sums, mov, cols, ids, a, b, n_workers=threads)
+        by_col = dict(zip(np.concatenate(calib).tolist(), secs.tolist()))
+        by_col.update(zip(cols.tolist(), secs2.tolist()))
+        for q, c, p in zip(buckets, calib, picks):
+            members = np.concatenate([c, p])
+            t = np.array([by_col[int(j)] for j in members])
+            total_cpu += float(t.mean()) * len(q)
+            sampled += len(members)
+        newton += int(st[2] + st2[2])
+    iter_s = total_cpu / threads
+    return 2.0 * V.nnz * r / iter_s, iter_s, sampled, newton / max(1, sampled * r)
 
 
 # ----------------------------------------------------------------------
@@ -222,19 +267,44 @@ def setup_dist(args):
     return world, rank, local
 
 
-def load_config(name):
+def load_config(name, device_matrix=False):
+    """(spec, V, w0, f0, generation seconds).  C1-C4 are generated on the host
+    (synth.generate).  C5's matrix (565M nonzeros) only exists on the device
+    (synth.generate_device): V is the DeviceMatrix when device_matrix is set,
+    else its host copy."""
     from paper_1604_04026_b200 import synth
 
     spec = synth.CONFIGS[name]
     t0 = time.perf_counter()
-    V = synth.generate(spec)
+    if name == "C5":
+        V = synth.generate_device(spec)
+        if not device_matrix:
+            V = V.to_host()
+    else:
+        V = synth.generate(spec)
     w0, f0 = synth.initial_factors(spec)
     return spec, V, w0, f0, time.perf_counter() - t0
 
 
+def ids_at(seed: int, r: int, iteration: int) -> np.ndarray:
+    """The reference's visit order of outer iteration `iteration` (1-based):
+    the iteration-th rng.permutation(r) of default_rng(seed) (solver.py:276,287)."""
+    rng = np.random.default_rng(seed)
+    for _ in range(iteration):
+        ids = rng.permutation(r).astype(np.int64)
+    return ids
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm on the host CPU (rank 0 only)."""
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """--impl reference: the reference algorithm on the host CPU (rank 0 only).
+
+    Warm-up: `warmup` full outer iterations of the reference algorithm from
+    the config's initial factors (oracle, support-t variant -- bitwise the
+    reference's iterates, at a fraction of the dense cost), which brings the
+    state to the one the GPU arm times (iteration warmup+1).  Each timed
+    step is then one stratified sample of the reference's per-column code
+    path (dense maintained product) at that state (cpu_reference_sample)."""
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -242,14 +312,26 @@ def run_reference(args):
 
     spec, V, w0, f0, _ = load_config(args.config)
     threads = oracle.cores()
-    per_step = max(2.0, min(args.cpu_seconds, 60.0) / max(1, args.steps + args.warmup) * 2)
-    for _ in range(args.warmup):
-        cpu_reference_sample(V, w0, f0, spec, per_step, threads)
-    vals, times = [], []
-    for _ in range(args.steps):
-        v, t_iter, sampled = cpu_reference_sample(V, w0, f0, spec, per_step, threads)
+    r, reg = spec.rank, spec.reg
+    t0 = time.perf_counter()
+    if args.warmup > 0:
+        st = oracle.drive(V.col_ptr, V.row_idx, V.values, spec.n, spec.m, w0, f0, r, reg.alpha1, reg.alpha2,
+                          reg.beta1, reg.beta2, args.warmup, spec.seed, n_workers=threads, log=False)
+        w, f = st["w"], st["f"]
+    else:
+        w, f = w0, f0
+    warm_s = time.perf_counter() - t0
+    ids = ids_at(spec.seed, r, args.warmup + 1)
+    vt = oracle.transpose_csc(V.n_rows, V.n_cols, V.col_ptr, V.row_idx, V.values)[:3]
+    vals, times, nsv = [], [], []
+    sampled = 0
+    for k in range(args.steps):
+        v, t_iter, n_s, steps_per_visit = cpu_reference_sample(V, w, f, spec, ids, args.cpu_seconds, threads,
+                                                               pick_seed=1000 + k, vt=vt)
         vals.append(v)
         times.append(t_iter)
+        nsv.append(steps_per_visit)
+        sampled += n_s
     value = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -259,9 +341,15 @@ def run_reference(args):
         "config": {"workload": spec.name, "n": spec.n, "m": spec.m, "nnz": V.nnz, "rank": spec.rank,
                    "reg": vars(spec.reg)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"stratified sample ({sampled} subproblems/step, both sides) of the "
-                                   f"reference sweep_range port (dense maintained product), extrapolated "
-                                   f"to a full outer iteration"},
+                         "sample": f"iteration {args.warmup + 1} state (after {args.warmup} full reference "
+                                   f"iterations, {warm_s:.0f} s); per step a stratified sample "
+                                   f"({sampled // max(1, args.steps)} subproblems, both sides, "
+                                   f"~{args.cpu_seconds:.0f} s on {threads} threads) of the reference "
+                                   f"sweep_range port (dense maintained product), per-column thread CPU "
+                                   f"time extrapolated by bucket population / {threads} cores",
+                         "iteration": args.warmup + 1,
+                         "newton_steps_per_visit": float(np.mean(nsv)),
+                         "step_values": [float(x) for x in vals]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -271,15 +359,18 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1604_04026_b200 import NmfConfig, factorize, FactorPair, DenseFactor
+    from paper_1604_04026_b200 import NmfConfig, factorize, FactorPair, DenseFactor, SparseMatrix
     from paper_1604_04026_b200.plan import DevicePlan
 
     world, rank, local = setup_dist(args)
     group = dist.group.WORLD if world > 1 else None
-    spec, V, w0, f0, gen_s = load_config(args.config)
+    spec, V, w0, f0, gen_s = load_config(args.config, device_matrix=True)
     precision = spec.precision
     dev = torch.device("cuda", local)
     plan = DevicePlan(V, spec.rank, precision, local, group)
+    if not isinstance(V, SparseMatrix):  # C5: host copy for the e2e / CPU legs (outside any timing)
+        V = V.to_host()
+        torch.cuda.empty_cache()
     plan.graph_after = 1  # timed steps replay captured graphs (captured during warm-up)
     r = spec.rank
     reg = spec.reg
@@ -292,21 +383,30 @@ def run_ours(args):
     kernel_ms = {}   # (side, kernel_id) -> list of ms
     launch_count = [0]
 
-    def step(events):
+    def step(events, mid=None):
         nonlocal ids
         ids_next = rng.permutation(r).astype(np.int64)
         plan.half_step("F", ids, alpha=reg.alpha2, beta=reg.beta2, events=events)
+        if mid is not None:
+            mid.record(stream)
         plan.half_step("W", ids, ids_next, alpha=reg.alpha1, beta=reg.beta1, events=events)
         ids = ids_next
 
     for _ in range(args.warmup):  # same (instrumented or not) graphs as the timed steps
         step(None if args.no_kernel_events else [])
     torch.cuda.synchronize(dev)
+    # the state of the first timed iteration, for the CPU baseline (read
+    # outside the timed region)
+    cpu_state = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+        w_st, f_st = plan.get_factors()
+        cpu_state = (w_st, f_st, ids.copy())
     if world > 1:
         dist.barrier()
 
     plan.take_stats()
     step_ms = []
+    half_ms = []  # (F half-step incl. its exchange, W half-step incl. its exchange) per timed step
     step_kernel_ms = []
     with ClockSampler(-1 if args.no_clocks else local) as clocks:
         for _ in range(args.steps):
@@ -315,17 +415,19 @@ def run_ours(args):
             ev = None if args.no_kernel_events else []
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            em = torch.cuda.Event(enable_timing=True)
             # ~1 ms device sleep outside [e0, e1]: the host enqueues the whole
             # step before the device reaches e0, so host latency after the
             # per-step synchronize is not counted as device time
             torch.cuda._sleep(2_000_000)
             e0.record(stream)
-            step(ev)
+            step(ev, em)
             e1.record(stream)
             # per-kernel events are CUDA-graph nodes re-recorded by each replay:
             # read them before the next step (device time is unaffected)
             torch.cuda.synchronize(dev)
             step_ms.append(e0.elapsed_time(e1))
+            half_ms.append((e0.elapsed_time(em), em.elapsed_time(e1)))
             ksum = 0.0
             for (side, kid, a, b) in ev or []:
                 kms = a.elapsed_time(b)
@@ -357,7 +459,25 @@ def run_ours(args):
         plan.concurrent = True
         plan.take_stats()
     total_ms = float(np.sum(step_ms))
+    # per-rank half-step times, the solver kernels' serialized time and the
+    # exchange volume (every rank sends its rows of the moving factor and, in
+    # fp32 mode, its entries' maintained products to every peer)
+    me = {"rank": rank, "f_half_ms": float(np.mean([h[0] for h in half_ms])),
+          "w_half_ms": float(np.mean([h[1] for h in half_ms])),
+          "kernel_ms_serialized": float(sum(np.sum(v) for v in kernel_ms.values())) / max(1, min(args.steps, 4))
+          if kernel_ms else None}
+    xb = {}
+    for side_name in ("F", "W"):
+        sp = plan.sides[side_name]
+        lo, hi = sp.ranges[rank]
+        ent = int(sp.ptr_host[hi] - sp.ptr_host[lo])
+        per_peer = (hi - lo) * plan.rp * (4 if plan.fp32 else 8) + (ent * 8 if plan.fp32 else 0)
+        xb[side_name] = {"items": hi - lo, "entries": ent, "bytes_sent": per_peer * (world - 1)}
+    me["exchange_per_half_step"] = xb
+    ranks_report = [me]
     if world > 1:
+        ranks_report = [None] * world
+        dist.all_gather_object(ranks_report, me)
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -405,7 +525,10 @@ def run_ours(args):
             "outer_iters_per_sec": 1e3 / ms_per_step,
             "config": {"workload": spec.name, "n": spec.n, "m": spec.m, "nnz": V.nnz, "rank": r,
                        "reg": vars(spec.reg), "precision": precision,
-                       "parallelism": f"dp{world} (nnz-balanced subproblem ranges, NCCL all-gather)",
+                       "parallelism": f"dp{world} (nnz-balanced subproblem ranges; exchange: "
+                                      + ("fused peer stores over NVLink (CUDA IPC), NCCL barrier"
+                                         if plan.fused_exchange else "NCCL all-gather" if world > 1 else "none")
+                                      + ")",
                        "l2": "flushed (256 MB write) before every timed step; V + maintained products "
                              "(~2.2 GB per half-step) exceed L2",
                        "gen_seconds": round(gen_s, 1)},
@@ -426,6 +549,7 @@ def run_ours(args):
                                       / ((spec.n + spec.m) * r),
                                       "cap_hits": st.cap_hits, "degenerate": st.degenerate},
             "gpu_launches": launch_count[0],
+            "ranks": ranks_report,
             "step_ms": [round(x, 3) for x in step_ms],
             "step_kernel_ms": [round(x, 3) for x in step_kernel_ms] if step_kernel_ms else None,
             "clocks": clocks.summary(),
@@ -446,7 +570,7 @@ def run_ours(args):
         # median of E2E_JOBS complete jobs: a single host-side stall (seen up
         # to ~1 s on the shared box hosts) would otherwise set the number
         job_s = []
-        for _ in range(E2E_JOBS):
+        for _ in range(args.e2e_jobs or (1 if spec.name == "C5" else E2E_JOBS)):
             torch.cuda.synchronize(dev)
             if world > 1:
                 dist.barrier()
@@ -471,15 +595,31 @@ def run_ours(args):
                            "includes": "upload of host CSC + factors, device CSR build and bucketing, "
                                        "iterations, download of both factors"}
 
-    if line is not None and not args.no_cpu and not args.profile and world == 1:
+    if line is not None and cpu_state is not None:
         import oracle
 
         threads = oracle.cores()
-        v, t_iter, sampled = cpu_reference_sample(V, w0, f0, spec, args.cpu_seconds, threads)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"{sampled} subproblems (stratified by nnz bucket, both sides) of "
-                                          f"the reference sweep_range port with its dense maintained "
-                                          f"product, extrapolated: {t_iter:.1f} s per outer iteration"}
+        w_st, f_st, ids_st = cpu_state
+        vt = oracle.transpose_csc(V.n_rows, V.n_cols, V.col_ptr, V.row_idx, V.values)[:3]
+        vals, times, nsv, sampled = [], [], [], 0
+        for k in range(args.cpu_samples):
+            v, t_iter, n_s, spv = cpu_reference_sample(V, w_st, f_st, spec, ids_st, args.cpu_seconds, threads,
+                                                       pick_seed=1000 + k, vt=vt)
+            vals.append(v)
+            times.append(t_iter)
+            nsv.append(spv)
+            sampled += n_s
+        line["cpu_baseline"] = {
+            "value": float(np.mean(vals)), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"state of timed iteration {args.warmup + 1} (the GPU's factors after warm-up); "
+                      f"{args.cpu_samples} stratified samples ({sampled // max(1, args.cpu_samples)} subproblems "
+                      f"each, both sides, ~{args.cpu_seconds:.0f} s on {threads} threads) of the reference "
+                      f"sweep_range port (dense maintained product), per-column thread CPU time extrapolated "
+                      f"by bucket population / {threads} cores: {float(np.mean(times)):.1f} s per outer iteration",
+            "iteration": args.warmup + 1,
+            "newton_steps_per_visit": float(np.mean(nsv)),
+            "gpu_newton_steps_per_visit": line["solver_stats_per_step"]["newton_steps_per_visit"],
+            "step_values": [float(x) for x in vals]}
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -489,6 +629,11 @@ def run_ours(args):
 
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     else:

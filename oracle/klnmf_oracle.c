@@ -21,7 +21,9 @@
  *                               identical: every ax[i] evolves independently and
  *                               is only read at S -- SURVEY.md finding 2)
  *   oracle_sweep                the reference's sweep() thread pool
- *                               (solver.py:165-216): equal-count column chunks
+ *                               (solver.py:165-216), columns handed out in blocks
+ *   oracle_sweep_cols_timed     sweep_range on a column sample with per-column
+ *                               thread CPU times (bench.py's CPU baseline)
  *   oracle_kl_data_term         _kernels.py:147-160
  *   oracle_row_sums             DenseFactor.row_sums (sparse.py:194-196) =
  *                               numpy's pairwise summation (SURVEY.md finding 8)
@@ -197,9 +199,18 @@ void oracle_sweep_range_support(const int64_t *col_ptr, const int64_t *row_idx, 
 }
 
 /* ------------------------------------------------------------------ */
-/* sweep(), solver.py:165-216: equal-count chunks (_chunk_bounds,
- * solver.py:160-162 = np.linspace(0, n, workers+1).astype(int64)), one
- * worker each, stats summed.  Results are worker-count invariant.       */
+/* sweep(), solver.py:165-216: the reference splits the columns into
+ * equal-count chunks (_chunk_bounds, solver.py:160-162 = np.linspace(0, n,
+ * workers+1).astype(int64)), one worker each, stats summed.  Results are
+ * invariant to how columns are assigned; with several workers the oracle
+ * hands out small column blocks dynamically (load balance on skewed sides). */
+/* Columns are independent and each is written by exactly one worker, so
+ * the result is identical for any assignment of columns to workers.  The
+ * reference's equal-count chunks leave one worker with all of a Zipf head's
+ * long rows (the W side of C3-C5 is essentially serial then), so workers
+ * here claim blocks of columns from a shared counter instead; `next` is
+ * NULL for the static equal-count chunk [j_lo, j_hi). */
+#define DYN_BLOCK 8
 typedef struct {
     const int64_t *col_ptr, *row_idx;
     const double *values, *at, *sum_a;
@@ -208,6 +219,7 @@ typedef struct {
     int64_t r, n_fix, n_mov, j_lo, j_hi, inner_cap, scratch;
     double alpha, beta, eps_grad, eps_x, eps_div;
     int local;
+    int64_t *next;
     int64_t stats[4];
 } sweep_task_t;
 
@@ -215,9 +227,20 @@ static void *sweep_worker(void *arg) {
     sweep_task_t *t = (sweep_task_t *)arg;
     double *ax = (double *)malloc(sizeof(double) * (size_t)(t->scratch > 0 ? t->scratch : 1));
     double *x = (double *)malloc(sizeof(double) * (size_t)t->r);
-    sweep_range_impl(t->col_ptr, t->row_idx, t->values, t->at, t->r, t->n_fix, t->sum_a, t->moving,
-                     t->n_mov, t->j_lo, t->j_hi, t->ids, t->alpha, t->beta, t->eps_grad, t->eps_x,
-                     t->eps_div, t->inner_cap, ax, x, t->stats, t->local);
+    if (!t->next) {
+        sweep_range_impl(t->col_ptr, t->row_idx, t->values, t->at, t->r, t->n_fix, t->sum_a, t->moving,
+                         t->n_mov, t->j_lo, t->j_hi, t->ids, t->alpha, t->beta, t->eps_grad, t->eps_x,
+                         t->eps_div, t->inner_cap, ax, x, t->stats, t->local);
+    } else {
+        for (;;) {
+            const int64_t a = __atomic_fetch_add(t->next, DYN_BLOCK, __ATOMIC_RELAXED);
+            if (a >= t->n_mov) break;
+            const int64_t b = a + DYN_BLOCK < t->n_mov ? a + DYN_BLOCK : t->n_mov;
+            sweep_range_impl(t->col_ptr, t->row_idx, t->values, t->at, t->r, t->n_fix, t->sum_a, t->moving,
+                             t->n_mov, a, b, t->ids, t->alpha, t->beta, t->eps_grad, t->eps_x, t->eps_div,
+                             t->inner_cap, ax, x, t->stats, t->local);
+        }
+    }
     free(ax);
     free(x);
     return NULL;
@@ -237,6 +260,7 @@ int oracle_sweep(const int64_t *col_ptr, const int64_t *row_idx, const double *v
     sweep_task_t *tasks = (sweep_task_t *)calloc((size_t)n_workers, sizeof(sweep_task_t));
     pthread_t *th = (pthread_t *)calloc((size_t)n_workers, sizeof(pthread_t));
     int n_tasks = 0;
+    int64_t next = 0; /* dynamic column blocks (see sweep_task_t) */
     for (int w = 0; w < n_workers; ++w) {
         /* np.linspace(0, n, W+1).astype(int64): floor of w*n/W in fp64 */
         int64_t a = (int64_t)((double)n_mov * (double)w / (double)n_workers);
@@ -248,6 +272,7 @@ int oracle_sweep(const int64_t *col_ptr, const int64_t *row_idx, const double *v
         t->j_lo = a; t->j_hi = b; t->inner_cap = inner_cap; t->scratch = local ? max_s : n_fix;
         t->alpha = alpha; t->beta = beta; t->eps_grad = eps_grad; t->eps_x = eps_x; t->eps_div = eps_div;
         t->local = local;
+        t->next = n_workers > 1 ? &next : NULL;
     }
     if (n_tasks == 1) {
         sweep_worker(&tasks[0]);
@@ -256,6 +281,83 @@ int oracle_sweep(const int64_t *col_ptr, const int64_t *row_idx, const double *v
         for (int i = 0; i < n_tasks; ++i) pthread_join(th[i], NULL);
     }
     for (int i = 0; i < n_tasks; ++i)
+        for (int q = 0; q < 4; ++q) stats_out[q] += tasks[i].stats[q];
+    free(tasks);
+    free(th);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* CPU-baseline sampler (bench.py): sweep_range on an explicit list of
+ * columns -- each solved exactly as sweep_range solves it, in place in
+ * `moving` -- with the thread CPU time of every column recorded, so a
+ * stratified sample extrapolates to a full half-step without depending on
+ * how well a small sample fills the worker threads.  Workers claim columns
+ * from a shared counter.                                                  */
+#include <time.h>
+
+typedef struct {
+    const int64_t *col_ptr, *row_idx, *cols;
+    const double *values, *at, *sum_a;
+    double *moving, *col_seconds;
+    const int64_t *ids;
+    int64_t r, n_fix, n_mov, n_cols, inner_cap, scratch;
+    double alpha, beta, eps_grad, eps_x, eps_div;
+    int local;
+    int64_t *next;
+    int64_t stats[4];
+} timed_task_t;
+
+static double thread_seconds(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_THREAD_CPUTIME_ID, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static void *timed_worker(void *arg) {
+    timed_task_t *t = (timed_task_t *)arg;
+    double *ax = (double *)malloc(sizeof(double) * (size_t)(t->scratch > 0 ? t->scratch : 1));
+    double *x = (double *)malloc(sizeof(double) * (size_t)t->r);
+    for (;;) {
+        const int64_t q = __atomic_fetch_add(t->next, 1, __ATOMIC_RELAXED);
+        if (q >= t->n_cols) break;
+        const int64_t j = t->cols[q];
+        const double t0 = thread_seconds();
+        sweep_range_impl(t->col_ptr, t->row_idx, t->values, t->at, t->r, t->n_fix, t->sum_a, t->moving,
+                         t->n_mov, j, j + 1, t->ids, t->alpha, t->beta, t->eps_grad, t->eps_x, t->eps_div,
+                         t->inner_cap, ax, x, t->stats, t->local);
+        t->col_seconds[q] = thread_seconds() - t0;
+    }
+    free(ax);
+    free(x);
+    return NULL;
+}
+
+int oracle_sweep_cols_timed(const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                            const double *at, int64_t r, int64_t n_fix, const double *sum_a, double *moving,
+                            int64_t n_mov, const int64_t *cols, int64_t n_cols, const int64_t *ids, double alpha,
+                            double beta, double eps_grad, double eps_x, double eps_div, int64_t inner_cap,
+                            int n_workers, int local, int64_t *stats_out, double *col_seconds) {
+    if (n_workers < 1) n_workers = 1;
+    int64_t max_s = 0;
+    for (int64_t q = 0; q < n_cols; ++q) {
+        const int64_t s = col_ptr[cols[q] + 1] - col_ptr[cols[q]];
+        if (s > max_s) max_s = s;
+    }
+    timed_task_t *tasks = (timed_task_t *)calloc((size_t)n_workers, sizeof(timed_task_t));
+    pthread_t *th = (pthread_t *)calloc((size_t)n_workers, sizeof(pthread_t));
+    int64_t next = 0;
+    for (int w = 0; w < n_workers; ++w) {
+        timed_task_t *t = &tasks[w];
+        t->col_ptr = col_ptr; t->row_idx = row_idx; t->cols = cols; t->values = values; t->at = at;
+        t->sum_a = sum_a; t->moving = moving; t->col_seconds = col_seconds; t->ids = ids; t->r = r;
+        t->n_fix = n_fix; t->n_mov = n_mov; t->n_cols = n_cols; t->inner_cap = inner_cap;
+        t->scratch = local ? max_s : n_fix; t->alpha = alpha; t->beta = beta; t->eps_grad = eps_grad;
+        t->eps_x = eps_x; t->eps_div = eps_div; t->local = local; t->next = &next;
+    }
+    for (int i = 0; i < n_workers; ++i) pthread_create(&th[i], NULL, timed_worker, &tasks[i]);
+    for (int i = 0; i < n_workers; ++i) pthread_join(th[i], NULL);
+    for (int i = 0; i < n_workers; ++i)
         for (int q = 0; q < 4; ++q) stats_out[q] += tasks[i].stats[q];
     free(tasks);
     free(th);

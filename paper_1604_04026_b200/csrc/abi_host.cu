@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,8 @@ cudaError_t ensure_smem(const void *fn, size_t bytes) {
     };
     static Entry cache[256];
     static int n = 0;
+    static std::mutex mu;  // host drop-ins run concurrently on the reference's worker threads
+    std::lock_guard<std::mutex> lock(mu);
     int dev = 0;
     cudaGetDevice(&dev);
     const void *key = static_cast<const char *>(fn) + dev;  // attributes are per device
@@ -91,6 +94,22 @@ struct DevBufs {
 };
 
 inline int32_t round_rp(int64_t r) { return (int32_t)((r + 3) / 4 * 4); }
+
+// Columns j_lo..j_hi-1 of an (r, n) C-order fp64 array: one strided copy
+// (r rows of (j_hi-j_lo) values, pitch n).  The device buffer is full-size;
+// its other columns are zeroed on upload so the layout transform reads no
+// uninitialised memory.
+cudaError_t copy_columns(double *dst, const double *src, int64_t r, int64_t n, int64_t j_lo, int64_t j_hi,
+                         cudaMemcpyKind kind, cudaStream_t st) {
+    if (r <= 0 || j_hi <= j_lo) return cudaSuccess;
+    if (kind == cudaMemcpyHostToDevice && j_hi - j_lo < n) {
+        const cudaError_t e = cudaMemsetAsync(dst, 0, sizeof(double) * (size_t)r * (size_t)n, st);
+        if (e != cudaSuccess) return e;
+    }
+    const size_t pitch = sizeof(double) * (size_t)n;
+    return cudaMemcpy2DAsync(dst + j_lo, pitch, src + j_lo, pitch, sizeof(double) * (size_t)(j_hi - j_lo),
+                             (size_t)r, kind, st);
+}
 
 }  // namespace
 }  // namespace klnmf
@@ -235,8 +254,10 @@ static int exact_host_call(const int64_t *col_ptr, const int64_t *row_idx, const
     }
     if (r * n_fix > 0)
         KLNMF_CHECK(cudaMemcpyAsync(d_at, at, sizeof(double) * r * n_fix, cudaMemcpyHostToDevice, st));
-    if (r * n_mov > 0)
-        KLNMF_CHECK(cudaMemcpyAsync(d_mov_ref, moving, sizeof(double) * r * n_mov, cudaMemcpyHostToDevice, st));
+    // Only columns j_lo..j_hi-1 of `moving` belong to this call: the reference
+    // runs disjoint column ranges concurrently on worker threads
+    // (solver.py:207-214), so the other columns are neither read nor written.
+    KLNMF_CHECK(copy_columns(d_mov_ref, moving, r, n_mov, j_lo, j_hi, cudaMemcpyHostToDevice, st));
     KLNMF_CHECK(cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * r, cudaMemcpyHostToDevice, st));
     KLNMF_CHECK(cudaMemcpyAsync(d_nat, nat.data(), sizeof(int32_t) * r, cudaMemcpyHostToDevice, st));
     KLNMF_CHECK(cudaMemcpyAsync(d_ident, ident.data(), sizeof(int32_t) * rp, cudaMemcpyHostToDevice, st));
@@ -294,8 +315,7 @@ static int exact_host_call(const int64_t *col_ptr, const int64_t *row_idx, const
     rc = klnmf_layout_from_device(d_moving, r, n_mov, d_order, rp, 0, d_mov_ref, st);
     if (rc) return rc;
     unsigned long long hs[KLNMF_STATS_LEN];
-    if (r * n_mov > 0)
-        KLNMF_CHECK(cudaMemcpyAsync(moving, d_mov_ref, sizeof(double) * r * n_mov, cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(copy_columns(moving, d_mov_ref, r, n_mov, j_lo, j_hi, cudaMemcpyDeviceToHost, st));
     KLNMF_CHECK(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
     KLNMF_CHECK(cudaStreamSynchronize(st));
     for (int q = 0; q < KLNMF_STATS_LEN; ++q) stats[q] += (int64_t)hs[q];
@@ -371,8 +391,7 @@ extern "C" int klnmf_mu_update_range(const int64_t *col_ptr, const int64_t *row_
     }
     if (r * n_fix > 0)
         KLNMF_CHECK(cudaMemcpyAsync(d_fix_ref, fixed, sizeof(double) * r * n_fix, cudaMemcpyHostToDevice, st));
-    if (r * n_mov > 0)
-        KLNMF_CHECK(cudaMemcpyAsync(d_mov_ref, moving, sizeof(double) * r * n_mov, cudaMemcpyHostToDevice, st));
+    KLNMF_CHECK(copy_columns(d_mov_ref, moving, r, n_mov, j_lo, j_hi, cudaMemcpyHostToDevice, st));
     KLNMF_CHECK(cudaMemcpyAsync(d_ident, ident.data(), sizeof(int32_t) * rp, cudaMemcpyHostToDevice, st));
     KLNMF_CHECK(cudaMemcpyAsync(d_sum, sum_pad.data(), sizeof(double) * rp, cudaMemcpyHostToDevice, st));
     iota_from<<<grid_for(j_hi - j_lo), 256, 0, st>>>(d_items, j_hi - j_lo, j_lo);
@@ -387,8 +406,7 @@ extern "C" int klnmf_mu_update_range(const int64_t *col_ptr, const int64_t *row_
     if (rc) return rc;
     rc = klnmf_layout_from_device(d_moving, r, n_mov, d_ident, rp, 0, d_mov_ref, st);
     if (rc) return rc;
-    if (r * n_mov > 0)
-        KLNMF_CHECK(cudaMemcpyAsync(moving, d_mov_ref, sizeof(double) * r * n_mov, cudaMemcpyDeviceToHost, st));
+    KLNMF_CHECK(copy_columns(moving, d_mov_ref, r, n_mov, j_lo, j_hi, cudaMemcpyDeviceToHost, st));
     KLNMF_CHECK(cudaStreamSynchronize(st));
     return 0;
 }

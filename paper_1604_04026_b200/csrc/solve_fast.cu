@@ -286,6 +286,13 @@ __device__ __forceinline__ void put_t(const klnmf_solve_args_t &a, int64_t i, do
     for (int p = 0; p < a.n_peers; ++p) a.peer_t[p][i] = v;
 }
 
+// After a thread's last peer store of the half-step: order its NVLink stores
+// before anything the host sequences after the kernel (the barrier that ends
+// the half-step is a stream-ordered collective on another device's queue).
+__device__ __forceinline__ void peer_fence(const klnmf_solve_args_t &a) {
+    if (a.n_peers > 0) __threadfence_system();
+}
+
 __device__ __forceinline__ void flush_stats(const Counters &cnt, bool lead, unsigned long long *stats, bool warp_sum) {
     if (!stats) return;
     unsigned ci = lead ? cnt.n_inner : 0u, cc = lead ? cnt.n_cap : 0u, cd = lead ? cnt.n_deg : 0u;
@@ -512,6 +519,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
         for (int e = 0; e < NPL; ++e)
             if (gl + e * L < s) put_t(a, lo + gl + e * L, entry_t(u[e], vi[e], pm.eps_div));
     }
+    peer_fence(a);
     flush_stats(cnt, gl == 0 && valid, a.stats, true);
     ph.mark(7);
     ph.flush(2, (threadIdx.x & 31) == 0);
@@ -694,6 +702,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
 #pragma unroll
     for (int e = 0; e < NPL; ++e)
         if (tid + e * NT < s) put_t(a, lo + tid + e * NT, entry_t(u[e], vi[e], pm.eps_div));
+    peer_fence(a);
     flush_stats(cnt, tid == 0, a.stats, false);
     ph.mark(7);
     ph.flush(3, tid == 0);
@@ -1117,6 +1126,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         const double2 uv = UVg[i];
         put_t(a, base + i, entry_t(uv.x, uv.y, eps));
     }
+    peer_fence(a);
     flush_stats(cnt, cq == 0 && tid == 0, a.stats, false);
     ph.mark(7);
     ph.flush(std::is_same<Reducer, CoopReducer>::value ? 1 : 0, threadIdx.x == 0);

@@ -83,6 +83,20 @@ def nnz_balanced_ranges(ptr: np.ndarray, parts: int):
     return [(bounds[q], bounds[q + 1]) for q in range(parts)]
 
 
+def _check_fp32_range(V) -> None:
+    """fp32 storage of V must keep every (positive) value a normal float:
+    below FLT_MIN it would round to 0 or a subnormal (1/v = inf, then NaN in
+    the entry state), above FLT_MAX to inf."""
+    vals = getattr(V, "values", None)
+    if not isinstance(vals, np.ndarray) or vals.size == 0:
+        return  # device matrices are generated in fp32 already
+    lo, hi = float(vals.min()), float(vals.max())
+    fi = np.finfo(np.float32)
+    if lo < float(fi.tiny) or hi > float(fi.max):
+        raise ValueError(f"V values span [{lo:g}, {hi:g}], outside the normal fp32 range "
+                         f"[{float(fi.tiny):g}, {float(fi.max):g}]; use precision='fp64'")
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -124,7 +138,9 @@ class DevicePlan:
             raise ValueError("the fp32 mode needs max(n, m) x padded rank < 2^31 (32-bit gather offsets); "
                              "use precision='fp64' or a smaller rank")
         self.order_mode = _lib.ORDER_COUNTER if order == "counter" else _lib.ORDER_SHARED
-        self.order_seed = int(order_seed) & (2**64 - 1)
+        self.order_seed = int(order_seed) & (2**64 - 1) if order == "counter" else 0
+        if precision == "fp32":
+            _check_fp32_range(V)
         if not torch.cuda.is_available():
             raise RuntimeError("DevicePlan needs a CUDA device (no CPU fallback)")
         _lib.load()

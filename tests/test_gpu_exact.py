@@ -30,6 +30,50 @@ def test_sweep_drop_in_bit_exact(cuda_ok, case):
     assert [st.cap_hits, st.degenerate, st.inner_iters, st.passes] == list(c["stats"])
 
 
+@pytest.mark.parametrize("n_workers", [3, 8])
+@pytest.mark.parametrize("case", range(0, len(SWEEP), 5))
+def test_sweep_drop_in_concurrent_workers(cuda_ok, case, n_workers):
+    """The reference drives sweep_range from a thread pool, one disjoint
+    column chunk per worker (solver.py:197-214); through the drop-in the
+    concurrent calls must each touch only their own columns, so the result
+    is bit-identical to the reference for any worker count."""
+    import paper_1604_04026_b200 as kb
+
+    c = SWEEP[case]
+    n_fix = int(c["n_fix"])
+    n_mov = c["moving_in"].shape[1]
+    V = kb.SparseMatrix(n_fix, n_mov, c["col_ptr"], c["row_idx"], c["values"])
+    moving = kb.DenseFactor(c["moving_in"].copy())
+    tol = kb.Tolerances(float(c["eps_grad"]), float(c["eps_x"]), float(c["eps_div"]), int(c["inner_cap"]))
+    st = kb.sweep(V, kb.DenseFactor(c["at"]), moving, c["sum_a"], c["ids"], float(c["alpha"]),
+                  float(c["beta"]), tol=tol, n_workers=n_workers)
+    assert np.array_equal(moving.values, c["moving_out"])
+    assert [st.cap_hits, st.degenerate, st.inner_iters, st.passes] == list(c["stats"])
+
+
+def test_sweep_range_writes_only_its_columns(cuda_ok):
+    """klnmf_sweep_range(j_lo, j_hi) leaves every other column of `moving`
+    untouched, even if the host copy changes during the call's lifetime
+    (another worker writing its chunk)."""
+    from paper_1604_04026_b200 import _lib
+
+    c = next(c for c in SWEEP if c["moving_in"].shape[1] >= 6 and c["col_ptr"][-1] > 0)
+    n_fix = int(c["n_fix"])
+    mv = c["moving_in"].copy()
+    r, n_mov = mv.shape
+    lo, hi = n_mov // 3, 2 * n_mov // 3
+    sentinel = np.full_like(mv, np.nan)
+    sentinel[:, lo:hi] = mv[:, lo:hi]
+    stats = np.zeros(4, dtype=np.int64)
+    ids = np.ascontiguousarray(c["ids"], dtype=np.int64)
+    args = [np.ascontiguousarray(c[k]) for k in ("col_ptr", "row_idx", "values", "at", "sum_a")]
+    _lib.call("klnmf_sweep_range", *[a.ctypes.data for a in args], sentinel.ctypes.data, lo, hi, ids.ctypes.data,
+              float(c["alpha"]), float(c["beta"]), float(c["eps_grad"]), float(c["eps_x"]), float(c["eps_div"]),
+              int(c["inner_cap"]), r, n_fix, n_mov, stats.ctypes.data)
+    assert np.isnan(sentinel[:, :lo]).all() and np.isnan(sentinel[:, hi:]).all()
+    assert np.array_equal(sentinel[:, lo:hi], c["moving_out"][:, lo:hi])
+
+
 @pytest.mark.parametrize("case", range(len(load_cases("objective_small.npz"))))
 def test_full_objective(cuda_ok, case):
     import paper_1604_04026_b200 as kb

@@ -133,3 +133,27 @@ def test_fp32_plan_rejects_32bit_offset_overflow():
     huge = types.SimpleNamespace(shape=(30_000_000, 10))
     with pytest.raises(ValueError, match="2\\^31"):
         DevicePlan(huge, 100, "fp32")
+
+
+@pytest.mark.parametrize("bad", [1e-40, 1e39])
+def test_fp32_plan_rejects_values_outside_normal_fp32(bad):
+    # a positive fp64 value that is subnormal/zero or inf in fp32 would make
+    # the entry state 1/v infinite and spread NaN: refused before any upload
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    V = kb.SparseMatrix(3, 2, np.array([0, 2, 3]), np.array([0, 2, 1]), np.array([1.0, bad, 2.0]))
+    with pytest.raises(ValueError, match="fp32 range"):
+        DevicePlan(V, 4, "fp32")
+
+
+def test_order_key_accepts_any_default_rng_seed():
+    # the reference accepts any seed default_rng does (solver.py:276); only
+    # the counter order needs a 64-bit key, derived deterministically
+    from paper_1604_04026_b200.solver import _order_key
+
+    assert _order_key(7) == 7 and _order_key(np.int64(9)) == 9
+    for seed in (None, [1, 2, 3], np.random.SeedSequence(5), 2**70):
+        k = _order_key(seed)
+        assert 0 <= k < 2**64
+        if seed is not None:
+            assert k == _order_key(seed)
