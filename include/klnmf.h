@@ -56,6 +56,10 @@ const char *klnmf_last_error(void);
 /* Counter-mode chunk order of one subproblem, computed on the host with the
  * device's generator (uint8 order[nchunks], nchunks <= 64). */
 int klnmf_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t nchunks, uint8_t *order);
+/* Counter-mode order of the 4 coordinates inside the chunk visited at
+ * position pos (uint8 perm[4]: slot c visits coordinate perm[c] of the
+ * chunk), computed on the host with the device's generator. */
+int klnmf_chunk_perm4(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t pos, uint8_t *perm);
 /* Record a CUDA event on a stream; external != 0 makes a recording inside a
  * CUDA-graph capture a real (timing-capable) event node, re-recorded by every
  * replay (used for per-kernel timing of captured half-steps). */
@@ -151,7 +155,8 @@ typedef struct {
     const int32_t *tmap;      /* nnz: index into t_in of each entry (NULL = identity) */
     const double *t_in;
     double *t_out;            /* nnz, entry order of this side */
-    double *scratch;          /* exact mode: nnz doubles; fp32 streaming bucket: 2*nnz */
+    double *scratch;          /* exact mode: nnz doubles; fp32 long-row kernels: 4*nnz (a 32-byte
+                                 record per entry, used only by entries beyond the on-chip capacity) */
     int32_t r;
     int32_t rp;
     double alpha, beta, eps_grad, eps_x, eps_div;

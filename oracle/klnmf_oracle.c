@@ -534,6 +534,28 @@ void oracle_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, uint32_t si
     }
 }
 
+/* Visit order of the 4 coordinates inside the chunk at visit position pos:
+ * Fisher-Yates over (0,1,2,3) from the top with word pos % 4 of the Philox
+ * block (0x100 + pos / 4, item, iter, side); step i takes the high word of
+ * word * (i+1) and continues with its low word.  perm[c] = coordinate of
+ * slot c. */
+void oracle_chunk_perm4(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t pos, uint8_t perm[4]) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const uint32_t ctr[4] = {0x100u + (uint32_t)(pos >> 2), item, iter, side};
+    uint32_t words[4];
+    oracle_philox4x32_10(ctr, key, words);
+    uint32_t word = words[pos & 3];
+    for (int i = 0; i < 4; ++i) perm[i] = (uint8_t)i;
+    for (int i = 3; i >= 1; --i) {
+        const uint64_t m = (uint64_t)word * (uint32_t)(i + 1);
+        const uint32_t j = (uint32_t)(m >> 32);
+        word = (uint32_t)m;
+        const uint8_t tmp = perm[i];
+        perm[i] = perm[j];
+        perm[j] = tmp;
+    }
+}
+
 static inline double round_f32(double x) {
     float f = (float)x;
     return f < FLT_MIN ? 0.0 : (double)f;
@@ -567,10 +589,14 @@ void oracle_sweep_fp32(const int64_t *ptr, const int32_t *idx, const float *val,
         }
         stats[STAT_PASSES] += 1;
         /* shared order: storage order; counter order: chunks in the
-         * subproblem's own order, storage order inside a chunk */
+         * subproblem's own order, and inside each chunk its own order of
+         * the 4 coordinates */
         if (order_mode) oracle_chunk_order(order_seed, order_iter, (uint32_t)j, order_side, nchunks, corder);
+        uint8_t perm4[4] = {0, 1, 2, 3};
         for (int64_t vis = 0; vis < (order_mode ? 4 * (int64_t)nchunks : r); ++vis) {
-            const int64_t tt = order_mode ? 4 * (int64_t)corder[vis / 4] + vis % 4 : vis;
+            if (order_mode && vis % 4 == 0)
+                oracle_chunk_perm4(order_seed, order_iter, (uint32_t)j, order_side, (int32_t)(vis / 4), perm4);
+            const int64_t tt = order_mode ? 4 * (int64_t)corder[vis / 4] + perm4[vis % 4] : vis;
             if (tt >= r) continue;
             double x = (double)moving[j * rp + tt];
             double g, h;

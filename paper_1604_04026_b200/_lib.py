@@ -33,6 +33,7 @@ EXPORTS = (
     "klnmf_ipc_open",
     "klnmf_ipc_close",
     "klnmf_chunk_order",
+    "klnmf_chunk_perm4",
     "klnmf_sweep_range",
     "klnmf_sweep_range_passes",
     "klnmf_kkt_violation",
@@ -139,6 +140,7 @@ _SIGS = {
     "klnmf_ipc_open": ([P, ctypes.POINTER(P)], INT),
     "klnmf_ipc_close": ([P], INT),
     "klnmf_chunk_order": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, I32, P], INT),
+    "klnmf_chunk_perm4": ([ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, I32, P], INT),
     "klnmf_sweep_range": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, P], INT),
     "klnmf_sweep_range_passes": ([P, P, P, P, P, P, I64, I64, P, D, D, D, D, D, I64, I64, I64, I64, I64, P], INT),
     "klnmf_kkt_violation": ([P, P, P, P, P, P, D, D, D, D, D, I64, I64, I64, P], INT),

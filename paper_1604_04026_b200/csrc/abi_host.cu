@@ -127,6 +127,14 @@ extern "C" int klnmf_chunk_order(uint64_t seed, uint32_t iter, uint32_t item, ui
     return 0;
 }
 
+extern "C" int klnmf_chunk_perm4(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int32_t pos,
+                                 uint8_t *perm) {
+    if (pos < 0 || pos >= klnmf::MAX_CHUNKS) return set_error_msg(1, "klnmf_chunk_perm4: 0 <= pos < 64");
+    const uint32_t p = klnmf::chunk_perm4(seed, iter, item, side, pos);
+    for (int c = 0; c < 4; ++c) perm[c] = (uint8_t)((p >> (2 * c)) & 3u);
+    return 0;
+}
+
 extern "C" int klnmf_event_create(void **event) {
     cudaEvent_t ev;
     KLNMF_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

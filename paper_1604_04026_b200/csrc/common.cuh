@@ -97,6 +97,31 @@ __host__ __device__ inline void chunk_order(uint64_t seed, uint32_t iter, uint32
     }
 }
 
+// Counter-mode visit order of the 4 coordinates inside the chunk visited at
+// position `pos` of subproblem `item`: Fisher-Yates over (0,1,2,3) from the
+// top, driven by word pos%4 of the Philox block with counter
+// (0x100 + pos/4, item, iter, side) -- disjoint from chunk_order's counters
+// (< 16); each step takes the high word of word*(i+1) and continues with the
+// low word.  Packed 2 bits per slot: slot c visits coordinate
+// (perm >> 2c) & 3 of the chunk.  Identical on host and device.
+constexpr uint32_t PERM4_IDENTITY = 0xE4u;  // 0 | 1<<2 | 2<<4 | 3<<6
+__host__ __device__ inline uint32_t chunk_perm4(uint64_t seed, uint32_t iter, uint32_t item, uint32_t side, int pos) {
+    uint32_t w[4] = {0x100u + (uint32_t)(pos >> 2), item, iter, side};
+    philox4x32_10(w, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const int wk = pos & 3;
+    uint32_t word = wk == 0 ? w[0] : (wk == 1 ? w[1] : (wk == 2 ? w[2] : w[3]));
+    uint32_t perm = PERM4_IDENTITY;
+    for (int i = 3; i >= 1; --i) {
+        const uint64_t m = (uint64_t)word * (uint32_t)(i + 1);
+        const uint32_t j = (uint32_t)(m >> 32);
+        word = (uint32_t)m;
+        const uint32_t a = (perm >> (2 * i)) & 3u, b = (perm >> (2 * j)) & 3u;
+        perm &= ~((3u << (2 * i)) | (3u << (2 * j)));
+        perm |= (b << (2 * i)) | (a << (2 * j));
+    }
+    return perm;
+}
+
 __device__ __forceinline__ float4 ldg_f4(const float *p) {
     return __ldg(reinterpret_cast<const float4 *>(p));
 }

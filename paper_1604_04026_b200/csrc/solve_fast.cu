@@ -441,16 +441,22 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
         const float4 *Ach = ring + (ch % STAGES) * NPL * NT + tid;  // own slots of this stage
         const int pc = phys(ch);  // per group in counter order
         const int nc = counter ? C : min(C, r - ch * C);
+        // counter order: this group's own order of the chunk's 4 coordinates
+        const uint32_t perm = counter ? chunk_perm4(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, ch)
+                                      : PERM4_IDENTITY;
         bool fresh = false;  // tot valid for the current t
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
-            const int tt = pc * C + cc;
+            const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
+            const int tt = pc * C + q;
             const bool live = tt < r;
             if (__any_sync(FULL_MASK, !fresh)) {
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                with_cc(cc, [&](auto ccv) {
+                // shared order: the chunk's remaining coordinates cc..C-1;
+                // counter order: all four (the remaining ones are any subset)
+                with_cc(counter ? 0 : cc, [&](auto ccv) {
 #pragma unroll
                     for (int e = 0; e < NPL; ++e)
                         accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], entry_z(u[e], vi[e]));
@@ -463,10 +469,10 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 ph.count(8);
                 fresh = true;
             }
-            double x = (double)xs[tt];
-            const double base = ssum[tt] + pm.beta;
-            double g = (base + pm.alpha * x) - tot[cc];
-            double h = pm.alpha + tot[C + cc];
+            double x = live ? (double)xs[tt] : 0.0;
+            const double base = (live ? ssum[tt] : 0.0) + pm.beta;
+            double g = (base + pm.alpha * x) - tot[q];
+            double h = pm.alpha + tot[C + q];
             int inner = 0;
             bool active = valid && live && enters(g, x, pm.eps_grad);
             bool moved = false;
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                     with_clamp(__any_sync(FULL_MASK, delta < 0.0), [&](auto cl) {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, cc)), pm.eps_div, u[e],
+                            entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, q)), pm.eps_div, u[e],
                                                               vi[e]);
                     });
                     ph.mark(5);
@@ -491,7 +497,7 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                     double g2 = 0.0, h2 = 0.0;
 #pragma unroll
                     for (int e = 0; e < NPL; ++e)
-                        accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, cc)));
+                        accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, q)));
 #pragma unroll
                     for (int o = L / 2; o > 0; o >>= 1) {
                         g2 += __shfl_xor_sync(FULL_MASK, g2, o);
@@ -632,16 +638,20 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
         ph.mark(1);
         const float4 *Ach = ring + (ch % STAGES) * NPL * NT + tid;
         const int pc = phys(ch);
-        const int nc = min(C, r - pc * C);
+        const int nc = counter ? C : min(C, r - pc * C);
+        const uint32_t perm = counter ? chunk_perm4(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, ch)
+                                      : PERM4_IDENTITY;
         bool fresh = false;
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
-            const int tt = pc * C + cc;
+            const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
+            const int tt = pc * C + q;
+            if (tt >= r) continue;  // counter order: padding slot of the last chunk
             if (!fresh) {  // block-uniform
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                with_cc(cc, [&](auto ccv) {
+                with_cc(counter ? 0 : cc, [&](auto ccv) {
 #pragma unroll
                     for (int e = 0; e < NPL; ++e)
                         accum_from<decltype(ccv)::value>(red, Ach[e * NT], u[e], entry_z(u[e], vi[e]));
@@ -656,8 +666,8 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
             }
             double x = (double)xs[tt];
             const double base = ssum[tt] + pm.beta;
-            double g = (base + pm.alpha * x) - bs.get(cur, cc);
-            double h = pm.alpha + bs.get(cur, C + cc);
+            double g = (base + pm.alpha * x) - bs.get(cur, q);
+            double h = pm.alpha + bs.get(cur, C + q);
             int inner = 0;
             bool active = enters(g, x, pm.eps_grad);
             bool moved = false;
@@ -671,7 +681,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                     with_clamp(delta < 0.0, [&](auto cl) {
 #pragma unroll
                         for (int e = 0; e < NPL; ++e)
-                            entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, cc)), pm.eps_div, u[e],
+                            entry_update<decltype(cl)::value>(delta, widen(comp(Ach + e * NT, q)), pm.eps_div, u[e],
                                                               vi[e]);
                     });
                 }
@@ -680,7 +690,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
                     double g2 = 0.0, h2 = 0.0;
 #pragma unroll
                     for (int e = 0; e < NPL; ++e)
-                        accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, cc)));
+                        accum(g2, h2, u[e], entry_z(u[e], vi[e]), widen(comp(Ach + e * NT, q)));
                     bs.reduce2(g2, h2, buf);
                     ph.mark(6);
                     ph.count(9);
@@ -727,6 +737,13 @@ constexpr int CL_NT = 256, CL_NR = 8, CL_NS = 8, CL_PER_SM = 2;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
 constexpr int CL_MAXG = 512;          // most CTAs in one cooperative row group
 constexpr size_t COOP_GROUP_BYTES = 2 * CL_MAXG * NV * 2 * sizeof(unsigned long long) + 128;
+
+// Per-entry record of the spilled entries of the long-row kernels (scratch).
+struct __align__(32) SpillRec {
+    double2 uv;  // u = v/(t+eps), vi = 1/v
+    float4 a;    // the current chunk of the entry's fixed-factor row
+};
+static_assert(sizeof(SpillRec) == 32, "one 32-byte sector per spilled entry");
 
 struct GroupRed {
     double wred[2][CL_NT / 32][NV];
@@ -947,8 +964,10 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const int64_t base = lo + c0;              // global entry index of local entry 0
     const double eps = pm.eps_div;
     // spilled entries (rows longer than the on-chip capacity of their CTAs):
-    // (u, vi) interleaved in scratch, one 16-byte access per entry
-    double2 *UVg = reinterpret_cast<double2 *>(a.scratch) + base;
+    // one 32-byte record per entry in scratch -- (u, vi) and the current
+    // chunk's 4 fixed-factor values, staged once per chunk -- so every pass
+    // and move streams whole sectors instead of re-gathering the fixed factor
+    SpillRec *UVg = reinterpret_cast<SpillRec *>(a.scratch) + base;
 
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
@@ -985,7 +1004,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         const int64_t g = base + i;
         double2 uv;
         entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, uv.x, uv.y);
-        UVg[i] = uv;
+        UVg[i].uv = uv;
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
@@ -1007,19 +1026,28 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         for (int e = 0; e < NS; ++e)
             cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + pc * C, offs[e] >= 0);
         cp_commit();
+        // spilled entries: stage the chunk's slice next to their state
+        // (each thread stages and later reads only its own records)
+#pragma unroll 4
+        for (int64_t i = spill0 + tid; i < cn; i += NT)
+            __stcg(&UVg[i].a, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C));
         cp_wait<0>();
         ph.mark(1);
         const float4 *A = cache + tid;
-        const int nc = min(C, r - pc * C);
+        const int nc = counter ? C : min(C, r - pc * C);
+        const uint32_t perm = counter ? chunk_perm4(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, ch)
+                                      : PERM4_IDENTITY;
         bool fresh = false;
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
-            const int tt = pc * C + cc;
+            const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
+            const int tt = pc * C + q;
+            if (tt >= r) continue;  // counter order: padding slot of the last chunk
             if (!fresh) {  // uniform over the group
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
-                with_cc(cc, [&](auto ccv) {
+                with_cc(counter ? 0 : cc, [&](auto ccv) {
                     constexpr int CC = decltype(ccv)::value;
 #pragma unroll
                     for (int e = 0; e < NR; ++e) accum_from<CC>(red, A[e * NT], u[e], entry_z(u[e], vi[e]));
@@ -1031,9 +1059,8 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                 });
 #pragma unroll 4
                 for (int64_t i = spill0 + tid; i < cn; i += NT) {
-                    const double2 uv = __ldcg(UVg + i);
-                    accum_chunk(red, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C), uv.x,
-                                entry_z(uv.x, uv.y), cc);
+                    const double2 uv = __ldcg(&UVg[i].uv);
+                    accum_chunk(red, __ldcg(&UVg[i].a), uv.x, entry_z(uv.x, uv.y), counter ? 0 : cc);
                 }
                 ph.mark(2);
                 reduce(red, buf);
@@ -1045,8 +1072,8 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             }
             double x = (double)xs[tt];
             const double sb = ssum[tt] + pm.beta;
-            double g = (sb + pm.alpha * x) - R.tot[cur][cc];
-            double h = pm.alpha + R.tot[cur][C + cc];
+            double g = (sb + pm.alpha * x) - R.tot[cur][q];
+            double h = pm.alpha + R.tot[cur][C + q];
             int inner = 0;
             bool active = enters(g, x, pm.eps_grad);
             bool moved = false;
@@ -1063,14 +1090,14 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                         constexpr bool CL = decltype(cl)::value;
 #pragma unroll
                         for (int e = 0; e < NR; ++e) {  // register entries: branch-free
-                            const double av = widen(comp(A + e * NT, cc));
+                            const double av = widen(comp(A + e * NT, q));
                             if (upd) entry_update<CL>(delta, av, eps, u[e], vi[e]);
                             if (again) accum(g2, h2, u[e], entry_z(u[e], vi[e]), av);
                         }
 #pragma unroll
                         for (int e = 0; e < NS; ++e) {
                             const int si = e * NT + tid;
-                            const double av = widen(comp(A + (NR + e) * NT, cc));
+                            const double av = widen(comp(A + (NR + e) * NT, q));
                             double uu = Us[si];
                             const double vv = VIs[si];
                             if (upd) {
@@ -1081,13 +1108,13 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                         }
 #pragma unroll 4
                         for (int64_t i = spill0 + tid; i < cn; i += NT) {
-                            const double av = (double)__ldg(fixed + (int64_t)a.side.idx[base + i] * rp + tt);
-                            double2 uv = __ldcg(UVg + i);
+                            const double av = (double)__ldcg(reinterpret_cast<const float *>(&UVg[i].a) + q);
+                            double2 uv = __ldcg(&UVg[i].uv);
                             double &uu = uv.x;
                             const double vv = uv.y;
                             if (upd) {
                                 entry_update<CL>(delta, av, eps, uu, vv);
-                                __stcg(UVg + i, uv);
+                                __stcg(&UVg[i].uv, uv);
                             }
                             if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
@@ -1123,7 +1150,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         if (offs[e] >= 0)
             put_t(a, base + tid + (int64_t)(NR + e) * NT, entry_t(Us[e * NT + tid], VIs[e * NT + tid], eps));
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
-        const double2 uv = UVg[i];
+        const double2 uv = UVg[i].uv;
         put_t(a, base + i, entry_t(uv.x, uv.y, eps));
     }
     peer_fence(a);

@@ -230,10 +230,10 @@ class DevicePlan:
                           "csr": torch.zeros(nz, dtype=torch.float64, device=dev)}
                 self._track("t", self.t["csc"], self.t["csr"])
                 # scratch backs per-entry state that cannot stay on chip (rows
-                # longer than the whole GPU's on-chip capacity, long-row bucket)
-                need_stream = any(b[0] == self._stream_kernel_id() and b[2] > 0
-                                  for s in self.sides.values() for b in s.buckets)
-                self.scratch = torch.empty(2 * nz if need_stream else 1, dtype=torch.float64, device=dev)
+                # longer than the whole GPU's on-chip capacity, long-row
+                # bucket): a 32-byte record per entry
+                need_spill = any(s.coop is not None and s.coop[5] for s in self.sides.values())
+                self.scratch = torch.empty(4 * nz if need_spill else 4, dtype=torch.float64, device=dev)
             else:
                 self.t = None
                 self.scratch = torch.empty(nz, dtype=torch.float64, device=dev)
@@ -440,7 +440,8 @@ class DevicePlan:
                     sched[wi, c0 + rank] = (q, rank, G, q)
         sched_d = torch.from_numpy(sched).to(self.dev)
         sync = torch.empty(count * group_bytes, dtype=torch.uint8, device=self.dev)
-        sp.coop = (sched_d, len(waves), n_ctas, sync, count)
+        spills = bool(np.any(sizes > n_ctas * per_cta))  # some row exceeds the whole GPU's on-chip capacity
+        sp.coop = (sched_d, len(waves), n_ctas, sync, count, spills)
 
     def _h2d_i32(self, dst: torch.Tensor, arr) -> None:
         host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32))
@@ -504,8 +505,9 @@ class DevicePlan:
         out[self.order[name]] = pos
         return out
 
-    def _init_t(self, which: str) -> None:
-        """t at every entry of one orientation = <W_i, F_j> from the stored factors."""
+    def _init_t(self, which: str, out: torch.Tensor | None = None) -> None:
+        """t at every entry of one orientation = <W_i, F_j> from the stored
+        factors (into the maintained products, or into `out`)."""
         side = self.sides["W"] if which == "csr" else self.sides["F"]
         fixed = self.factors["F"] if which == "csr" else self.factors["W"]
         moving = self.factors["W"] if which == "csr" else self.factors["F"]
@@ -515,9 +517,21 @@ class DevicePlan:
         self._h2d_i32(self._pos[1], self._padded(np.argsort(mo)))
         s = side.side_struct()
         _lib.call("klnmf_init_t", ctypes.byref(s), fixed.data_ptr(), moving.data_ptr(), self.rp,
-                  self._pos[0].data_ptr(), self._pos[1].data_ptr(), self.r, self.t[which].data_ptr(),
-                  self.stream_ptr)
-        self.t_current = which
+                  self._pos[0].data_ptr(), self._pos[1].data_ptr(), self.r,
+                  (self.t[which] if out is None else out).data_ptr(), self.stream_ptr)
+        if out is None:
+            self.t_current = which
+
+    def products_from_factors(self) -> torch.Tensor:
+        """fp32 mode: <W_i, F_j> recomputed from the stored factors at every
+        entry, in the orientation of the current maintained products (a
+        fresh tensor; the carried products are untouched) -- for checking
+        the carried t against the factors."""
+        if not self.fp32 or self.t_current is None:
+            raise RuntimeError("no maintained products are carried (fp32 mode, after a half-step)")
+        out = torch.empty_like(self.t[self.t_current])
+        self._init_t(self.t_current, out)
+        return out
 
     # kernels launched per outer iteration besides the solver buckets:
     # the fast row sums are two launches per half-step
@@ -546,6 +560,13 @@ class DevicePlan:
         is the counter of the per-subproblem chunk orders (it travels with the
         maps, so the captured graphs stay valid).
         """
+        torch.cuda.nvtx.range_push(f"klnmf.half_step.{which}")
+        try:
+            self._half_step(which, ids, ids_next, alpha, beta, tol, sums_pos, events, iteration)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    def _half_step(self, which, ids, ids_next, alpha, beta, tol, sums_pos, events, iteration) -> None:
         if self.order_mode == _lib.ORDER_COUNTER and iteration is None:
             raise ValueError("the counter coordinate order needs the iteration number")
         if self.fp32 and not tol.eps_div > 0.0:
@@ -593,7 +614,9 @@ class DevicePlan:
             self.t_current = "csc" if which == "F" else "csr"
         self.order[which] = np.asarray(out_order, dtype=np.int64).copy()
         if self.world > 1:
+            torch.cuda.nvtx.range_push(f"klnmf.exchange.{which}")
             self._exchange(which)
+            torch.cuda.nvtx.range_pop()
 
     def _stage_perms(self, host: np.ndarray) -> None:
         """Visit-order maps -> device through a pinned buffer (no host stall).
@@ -707,7 +730,7 @@ class DevicePlan:
             if not self.fp32:
                 _lib.check(lib.klnmf_solve_exact(ctypes.byref(a), sptr), "klnmf_solve_exact")
             elif kid == coop_kid:
-                sched, n_waves, n_ctas, sync, n_groups = side.coop
+                sched, n_waves, n_ctas, sync, n_groups, _ = side.coop
                 _lib.check(lib.klnmf_solve_coop(ctypes.byref(a), sched.data_ptr(), n_waves, n_ctas,
                                                 sync.data_ptr(), n_groups, sptr), "klnmf_solve_coop")
             else:
@@ -763,10 +786,21 @@ class DevicePlan:
             arr = t.cpu().numpy()
         return SolveStats.from_array(arr)
 
-    def objective(self, alpha1=0.0, alpha2=0.0, beta1=0.0, beta2=0.0, eps_div=1e-16):
-        """(kl, total, sparsity_w, sparsity_f) -- full_objective, solver.py:219-234."""
+    def objective(self, alpha1=0.0, alpha2=0.0, beta1=0.0, beta2=0.0, eps_div=1e-16, from_factors=False):
+        """(kl, total, sparsity_w, sparsity_f) -- full_objective, solver.py:219-234.
+
+        fp32 mode reads the data term from the carried maintained products
+        (one streaming pass); ``from_factors=True`` recomputes it from the
+        stored factors with an r-dot per nonzero, as the reference does."""
+        torch.cuda.nvtx.range_push("klnmf.objective")
+        try:
+            return self._objective(alpha1, alpha2, beta1, beta2, eps_div, from_factors)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    def _objective(self, alpha1, alpha2, beta1, beta2, eps_div, from_factors):
         data = ctypes.c_double()
-        if self.fp32 and self.t_current is not None:
+        if self.fp32 and self.t_current is not None and not from_factors:
             # fp32 mode carries t = <W_i, F_j> for every entry (all ranks hold all
             # of it after the exchange): one streaming pass over (v, t)
             side = self.sides["F"] if self.t_current == "csc" else self.sides["W"]

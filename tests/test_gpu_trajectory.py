@@ -1,0 +1,102 @@
+"""fp32 throughput mode against the reference algorithm at BASELINE.json's
+full sizes, every outer iteration (north-star bar: KL objective trajectory
+within 1e-4 relative at every outer iteration).
+
+The reference trajectories are committed fixtures (tests/golden/
+make_trajectories.py: the reference loop, solver.py:283-317, run for the
+config's iteration count on the pinned CPU oracle from the same
+fp32-representable start).  The GPU runs the same loop on a DevicePlan in
+fp32 mode (what ``factorize(precision="fp32")`` drives, solver.py of this
+package) and at every iteration also checks its own bookkeeping against the
+factors it stores:
+
+  * the logged objective (read from the carried maintained products t)
+    against the objective recomputed from the stored factors (an r-dot per
+    nonzero, _kernels.kl_data_term's formula, _kernels.py:147-160);
+  * every carried t against <W_i, F_j> recomputed from the stored factors.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+TRAJ_RTOL = 1e-4         # north-star bar
+OBJ_T_VS_FACTORS = 1e-9  # carried-t objective vs factor-derived objective
+T_REL = 1e-9             # carried t vs <W_i, F_j>, relative to max(t, median t * 1e-6)
+
+
+def _matrix_sha(V) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(V.col_ptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(V.row_idx, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(V.values, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def _fixture(name):
+    path = GOLDEN / f"{name.lower()}_traj_full.npz"
+    if not path.exists():
+        pytest.fail(f"missing fixture {path.name} (tests/golden/make_trajectories.py {name})")
+    return dict(np.load(path, allow_pickle=False))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_trajectory_matches_reference(cuda_ok, name):
+    import torch
+
+    from paper_1604_04026_b200 import synth
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    g = _fixture(name)
+    spec = synth.CONFIGS[name]
+    iters = int(g["iters"])
+    if bool(g["device_generated"]):
+        Vd = synth.generate_device(spec)
+        V = Vd.to_host()
+    else:
+        Vd = None
+        V = synth.generate(spec)
+    assert V.nnz == int(g["nnz"])
+    assert _matrix_sha(V) == str(g["matrix_sha"]), "generator output changed: regenerate the fixture"
+    w0, f0 = synth.initial_factors(spec)
+    assert hashlib.sha256(w0.tobytes()).hexdigest() == str(g["w0_sha"])
+    plan = DevicePlan(Vd if Vd is not None else V, spec.rank, "fp32")
+    del Vd
+    reg = spec.reg
+    rng = np.random.default_rng(spec.seed)
+    ids = rng.permutation(spec.rank).astype(np.int64)
+    plan.set_factors(w0, f0, order=ids)
+    del w0, f0
+    kl, total, kl_f, worst_t = [], [], [], []
+    for it in range(iters):
+        assert np.array_equal(ids, g["ids"][it])
+        ids_next = rng.permutation(spec.rank).astype(np.int64)
+        plan.half_step("F", ids, alpha=reg.alpha2, beta=reg.beta2)
+        plan.half_step("W", ids, ids_next, alpha=reg.alpha1, beta=reg.beta1)
+        ids = ids_next
+        k, t, _, _ = plan.objective(reg.alpha1, reg.alpha2, reg.beta1, reg.beta2)
+        kf, tf, _, _ = plan.objective(reg.alpha1, reg.alpha2, reg.beta1, reg.beta2, from_factors=True)
+        kl.append(k)
+        total.append(t)
+        kl_f.append(kf)
+        carried = plan.t[plan.t_current][: plan.nnz]
+        fresh = plan.products_from_factors()[: plan.nnz]
+        floor = float(torch.median(fresh)) * 1e-6
+        worst_t.append(float(((carried - fresh).abs() / torch.clamp(fresh, min=floor)).max()))
+        del fresh
+    kl, total, kl_f, worst_t = map(np.array, (kl, total, kl_f, worst_t))
+    rel_kl = np.abs(kl - g["kl"]) / np.abs(g["kl"])
+    rel_total = np.abs(total - g["total"]) / np.abs(g["total"])
+    rel_obj = np.abs(kl - kl_f) / np.abs(kl_f)
+    print(f"{name}: {iters} its, max rel kl {rel_kl.max():.2e} total {rel_total.max():.2e}; "
+          f"t-objective vs factors {rel_obj.max():.2e}; carried t vs <W,F> {worst_t.max():.2e}")
+    assert np.all(rel_kl <= TRAJ_RTOL) and np.all(rel_total <= TRAJ_RTOL), (rel_kl, rel_total)
+    assert np.all(rel_obj <= OBJ_T_VS_FACTORS), rel_obj
+    assert np.all(worst_t <= T_REL), worst_t
+    del plan
+    torch.cuda.empty_cache()

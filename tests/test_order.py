@@ -78,3 +78,37 @@ def test_counter_order_is_fp32_only():
     with pytest.raises(ValueError):
         NmfConfig(precision="fp32", order="random")
     NmfConfig(precision="fp32", order="counter")
+
+
+def _lib_perm4(seed, it, item, side, pos):
+    from paper_1604_04026_b200 import _lib
+
+    out = (ctypes.c_uint8 * 4)()
+    _lib.call("klnmf_chunk_perm4", seed, it, item, side, pos, out)
+    return np.frombuffer(out, dtype=np.uint8).copy()
+
+
+def test_library_in_chunk_orders_match_oracle():
+    rng = np.random.default_rng(5)
+    for _ in range(500):
+        seed = int(rng.integers(0, 2**63))
+        it, item = (int(x) for x in rng.integers(0, 2**31, size=2))
+        side, pos = int(rng.integers(0, 2)), int(rng.integers(0, 64))
+        a = _lib_perm4(seed, it, item, side, pos)
+        assert np.array_equal(a, oracle.chunk_perm4(seed, it, item, side, pos))
+        assert np.array_equal(np.sort(a), np.arange(4))
+
+
+def test_in_chunk_orders_cover_all_24_uniformly():
+    """Each subproblem gets its own order inside every chunk: over many
+    subproblems all 24 permutations of a chunk's coordinates occur ~equally."""
+    from collections import Counter
+
+    items = 24000
+    c = Counter(tuple(oracle.chunk_perm4(9, 3, j, 1, 7)) for j in range(items))
+    assert len(c) == 24
+    expected = items / 24
+    chi2 = sum((v - expected) ** 2 / expected for v in c.values())
+    assert chi2 < 60, chi2  # 23 degrees of freedom; p ~ 5e-5 at 60
+    # and orders differ between chunks of one subproblem
+    assert len({tuple(oracle.chunk_perm4(9, 3, 11, 1, p)) for p in range(25)}) > 5
