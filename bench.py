@@ -469,10 +469,10 @@ def run_ours(args):
     xb = {}
     for side_name in ("F", "W"):
         sp = plan.sides[side_name]
-        lo, hi = sp.ranges[rank]
-        ent = int(sp.ptr_host[hi] - sp.ptr_host[lo])
-        per_peer = (hi - lo) * plan.rp * (4 if plan.fp32 else 8) + (ent * 8 if plan.fp32 else 0)
-        xb[side_name] = {"items": hi - lo, "entries": ent, "bytes_sent": per_peer * (world - 1)}
+        mine = sp.owned_items(rank)
+        ent = int(np.diff(sp.ptr_host)[mine].sum())
+        per_peer = len(mine) * plan.rp * (4 if plan.fp32 else 8) + (ent * 8 if plan.fp32 else 0)
+        xb[side_name] = {"items": int(len(mine)), "entries": ent, "bytes_sent": per_peer * (world - 1)}
     me["exchange_per_half_step"] = xb
     ranks_report = [me]
     if world > 1:

@@ -83,6 +83,78 @@ def nnz_balanced_ranges(ptr: np.ndarray, parts: int):
     return [(bounds[q], bounds[q + 1]) for q in range(parts)]
 
 
+# Per-entry cost (ns per entry per half-step, one B200) of the fp32 bucket
+# kernels by subproblem size, measured at C4 (bench.py kernel table, buckets
+# launched one at a time): the warp/block kernels ~0.22-0.26,
+# the cluster kernels 0.35 (2 CTAs) to 0.51 (16 CTAs), the cooperative kernel
+# 0.48; entries beyond the whole GPU's on-chip capacity (the spill path) cost
+# SPILL_NS each.  Every subproblem also pays ITEM_NS of per-coordinate work.
+COST_EDGES = np.array([4096, 8192, 16384, 32768, 65536], dtype=np.int64)
+COST_NS = np.array([0.24, 0.35, 0.38, 0.44, 0.51, 0.48])
+ITEM_NS = 15.0
+SPILL_NS = 1.2
+ON_CHIP_ENTRIES = 296 * 4096  # cooperative kernel: CTAs x entries per CTA
+
+
+def subproblem_cost(sizes: np.ndarray) -> np.ndarray:
+    """Modelled device time (ns) of each subproblem of a half-step."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    per = COST_NS[np.searchsorted(COST_EDGES, sizes, side="left")]
+    spill = np.maximum(sizes - ON_CHIP_ENTRIES, 0)
+    return ITEM_NS + per * (sizes - spill) + SPILL_NS * spill
+
+
+def cost_balanced_ranges(ptr: np.ndarray, parts: int, cost=subproblem_cost):
+    """Contiguous item ranges [lo, hi) with about equal modelled device time
+    (items atomic).  Balancing by nnz alone hands the first rank the Zipf
+    head's long rows, whose per-entry cost is about twice the short ones'."""
+    ptr = np.asarray(ptr, dtype=np.int64)
+    n = ptr.shape[0] - 1
+    if parts <= 1 or n == 0:
+        return [(0, n)] + [(n, n)] * max(parts - 1, 0)
+    c = np.concatenate([[0.0], np.cumsum(cost(np.diff(ptr)))])
+    bounds = [0]
+    for q in range(1, parts):
+        b = int(np.searchsorted(c, c[-1] * q / parts, side="left"))
+        # the item straddling the target goes to whichever side is closer
+        if 0 < b <= n and (c[b] - c[-1] * q / parts) > (c[-1] * q / parts - c[b - 1]):
+            b -= 1
+        bounds.append(min(max(b, bounds[-1]), n))
+    bounds.append(n)
+    return [(bounds[q], bounds[q + 1]) for q in range(parts)]
+
+
+def dealt_assignment(ptr: np.ndarray, parts: int, cost=subproblem_cost, heavy_frac: float = 0.25):
+    """Items of each rank (sorted ascending), balancing modelled device time
+    when items need not be contiguous (the fused peer exchange stores every
+    result by item): items costing more than heavy_frac x the mean rank load
+    -- the Zipf head's long rows -- are dealt largest first to the least
+    loaded rank; the others are cut, in item order, into runs that fill each
+    rank up to the mean."""
+    ptr = np.asarray(ptr, dtype=np.int64)
+    n = ptr.shape[0] - 1
+    if parts <= 1:
+        return [np.arange(n, dtype=np.int64)]
+    c = cost(np.diff(ptr))
+    target = float(c.sum()) / parts
+    owner = np.full(n, -1, dtype=np.int64)
+    loads = np.zeros(parts)
+    heavy = np.nonzero(c > heavy_frac * target)[0]
+    for i in heavy[np.argsort(-c[heavy], kind="stable")]:
+        q = int(np.argmin(loads))
+        owner[i] = q
+        loads[q] += c[i]
+    light = np.nonzero(owner < 0)[0]
+    if light.size:
+        room = np.maximum(target - loads, 0.0)
+        if room.sum() <= 0.0:
+            room = np.ones(parts)
+        cl = np.cumsum(c[light])
+        cuts = np.searchsorted(cl, np.cumsum(room / room.sum() * cl[-1])[:-1], side="left")
+        owner[light] = np.searchsorted(cuts, np.arange(light.size), side="right")
+    return [np.nonzero(owner == q)[0] for q in range(parts)]
+
+
 def _check_fp32_range(V) -> None:
     """fp32 storage of V must keep every (positive) value a normal float:
     below FLT_MIN it would round to 0 or a subnormal (1/v = inf, then NaN in
@@ -111,11 +183,19 @@ class SidePlan:
     n_mov: int
     nnz: int
     ptr_host: np.ndarray
-    ranges: list              # per-rank [lo, hi)
+    ranges: list | None       # per-rank [lo, hi) (contiguous ownership), or None
     items: torch.Tensor       # int32, this rank's items, sorted by nnz descending
     buckets: list             # [(kernel_id, start, count)], largest first
     tmap: torch.Tensor | None = None  # int32[nnz] entry -> position in the other side
-    coop: tuple | None = None  # long-row bucket: (schedule, n_waves, n_ctas, sync, n_groups)
+    coop: tuple | None = None  # long-row bucket: (schedule, n_waves, n_ctas, sync, n_groups, spills)
+    owned: list | None = None  # per-rank item arrays (dealt ownership), or None
+
+    def owned_items(self, rank: int) -> np.ndarray:
+        """Items rank `rank` solves in this side's half-steps."""
+        if self.owned is not None:
+            return self.owned[rank]
+        lo, hi = self.ranges[rank]
+        return np.arange(lo, hi, dtype=np.int64)
 
     def side_struct(self) -> _lib.Side:
         return _lib.Side(self.ptr.data_ptr(), self.idx.data_ptr(), self.val.data_ptr(),
@@ -202,6 +282,11 @@ class DevicePlan:
 
             tick("transpose")
             self.fast_kernels = fast_kernels if fast_kernels is not None else _lib.fast_kernels(self.rp)
+            if fused_exchange is None:
+                fused_exchange = os.environ.get("KLNMF_FUSED_EXCHANGE", "1") != "0"
+            # the fused exchange stores every result by item, so sharded fp32
+            # runs may own any item set: long rows are dealt across ranks
+            self._dealt = self.world > 1 and self.fp32 and bool(fused_exchange)
             self.sides = {
                 "F": self._make_side("F", csc_ptr, csc_idx, csc_val, self.n, self.m, col_ptr_host,
                                      map_csc2csr if self.fp32 else None),
@@ -265,11 +350,18 @@ class DevicePlan:
             # stores through CUDA IPC) unless disabled; fp64 all-gathers
             self._peers = None
             self._ipc_bases = []
-            if fused_exchange is None:
-                fused_exchange = os.environ.get("KLNMF_FUSED_EXCHANGE", "1") != "0"
             if self.world > 1 and self.fp32 and fused_exchange:
                 self._setup_peers()
                 tick("peer mappings")
+                if self._peers is None and self._dealt:
+                    # the NCCL all-gather moves contiguous ranges: re-split
+                    self._dealt = False
+                    for name, sp in list(self.sides.items()):
+                        self.sides[name] = self._make_side(name, sp.ptr, sp.idx, sp.val, sp.n_fix, sp.n_mov,
+                                                           sp.ptr_host, sp.tmap)
+                        self._build_coop(self.sides[name])
+                    if any(sp.coop is not None and sp.coop[5] for sp in self.sides.values()):
+                        self.scratch = torch.empty(4 * max(self.nnz, 1), dtype=torch.float64, device=dev)
 
     # ------------------------------------------------------------------
     @staticmethod
@@ -385,8 +477,16 @@ class DevicePlan:
         return -1
 
     def _make_side(self, name, ptr, idx, val, n_fix, n_mov, ptr_host, tmap) -> SidePlan:
-        ranges = nnz_balanced_ranges(ptr_host, self.world)
-        lo, hi = ranges[self.rank_id]
+        ptr_host = np.asarray(ptr_host, dtype=np.int64)
+        ranges, owned = None, None
+        if self._dealt:
+            owned = dealt_assignment(ptr_host, self.world)
+            mine = owned[self.rank_id]
+            n_mine = int(mine.size)
+        else:
+            ranges = (cost_balanced_ranges if self.fp32 else nnz_balanced_ranges)(ptr_host, self.world)
+            lo, hi = ranges[self.rank_id]
+            n_mine = hi - lo
         if self.fp32:
             caps = [c for _, c, _, _ in self.fast_kernels]
             bounds = np.array([c if c >= 0 else INT64_MAX for c in caps], dtype=np.int64)
@@ -394,10 +494,17 @@ class DevicePlan:
         else:
             bounds = np.array([INT64_MAX], dtype=np.int64)
             kids = [-1]
-        items = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=self.dev)
+        items = torch.empty(max(n_mine, 1), dtype=torch.int32, device=self.dev)
         counts = np.zeros(len(bounds), dtype=np.int64)
-        _lib.call("klnmf_bucketize", ptr.data_ptr(), lo, hi, bounds.ctypes.data, len(bounds),
-                  items.data_ptr(), counts.ctypes.data, self.stream_ptr)
+        if owned is None:
+            _lib.call("klnmf_bucketize", ptr.data_ptr(), lo, hi, bounds.ctypes.data, len(bounds),
+                      items.data_ptr(), counts.ctypes.data, self.stream_ptr)
+        elif n_mine:
+            # the device bucketize's order: size descending, ties by item
+            sz = np.diff(ptr_host)[mine]
+            order = np.argsort(-sz, kind="stable")
+            items.copy_(torch.from_numpy(mine[order].astype(np.int32)))
+            counts[:] = np.bincount(np.searchsorted(bounds, sz, side="left"), minlength=len(bounds))
         # items are sorted by nnz descending: the largest bucket comes first
         buckets = []
         start = 0
@@ -405,9 +512,9 @@ class DevicePlan:
             c = int(counts[b])
             buckets.append((kids[b], start, c))
             start += c
-        assert start == hi - lo, (start, hi, lo)
+        assert start == n_mine, (start, n_mine)
         return SidePlan(name, ptr, idx, val, int(n_fix), int(n_mov), int(ptr[-1].item()) if n_mov else 0,
-                        np.asarray(ptr_host, dtype=np.int64), ranges, items, buckets, tmap)
+                        ptr_host, ranges, items, buckets, tmap, owned=owned)
 
     def _build_coop(self, sp: SidePlan) -> None:
         """Pack the long-row bucket into waves of the cooperative kernel.

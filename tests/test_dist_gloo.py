@@ -127,3 +127,81 @@ def test_sharded_half_steps_bitwise_rank_invariant():
     for _, w, f in pair:
         assert np.array_equal(w, single[1])
         assert np.array_equal(f, single[2])
+
+
+def _c5_like_row_sizes():
+    """Row lengths with C5's shape: Zipf(1.0)
+    feature popularity over 141,043 rows, 8.2M documents, ~565M nonzeros,
+    longest rows ~7M (a row cannot exceed the document count)."""
+    i = np.arange(1, 141_044, dtype=np.float64)
+    m = 8.2e6
+    lo, hi = 0.1, 100.0
+    for _ in range(60):  # expected tokens of the top feature per document
+        c = np.sqrt(lo * hi)
+        tot = (m * -np.expm1(-c / i)).sum()
+        lo, hi = (c, hi) if tot < 5.65e8 else (lo, c)
+    return np.maximum(1, (m * -np.expm1(-c / i))).astype(np.int64)
+
+
+def test_cost_balanced_ranges_properties():
+    from paper_1604_04026_b200.plan import cost_balanced_ranges, subproblem_cost
+
+    rng = np.random.default_rng(4)
+    sizes = rng.zipf(1.3, size=5000).clip(max=2_000_000)
+    ptr = np.concatenate([[0], np.cumsum(sizes)])
+    cost = subproblem_cost(sizes)
+    for parts in (1, 2, 3, 8):
+        rs = cost_balanced_ranges(ptr, parts)
+        assert rs[0][0] == 0 and rs[-1][1] == len(sizes)
+        assert all(a[1] == b[0] and a[0] <= a[1] for a, b in zip(rs, rs[1:]))
+        loads = [cost[lo:hi].sum() for lo, hi in rs]
+        assert max(loads) <= cost.sum() / parts + cost.max()
+
+
+def test_cost_balancing_c5_w_side_at_8_ranks():
+    """C5's W side (rows, Zipf head first): nnz-balanced ranges give the first
+    rank the long rows (spill path, ~2-5x the per-entry cost), cost-balanced
+    ranges keep the modelled per-rank time within 10% of the mean at P=8
+    (DESIGN.md §6)."""
+    from paper_1604_04026_b200.plan import (cost_balanced_ranges, dealt_assignment, nnz_balanced_ranges,
+                                            subproblem_cost)
+
+    sizes = _c5_like_row_sizes()
+    assert 5.5e8 < sizes.sum() < 5.8e8 and 6e6 < sizes.max() < 8.2e6
+    ptr = np.concatenate([[0], np.cumsum(sizes)])
+    cost = subproblem_cost(sizes)
+
+    def imbalance(rs):
+        loads = np.array([cost[lo:hi].sum() for lo, hi in rs])
+        return loads.max() / loads.mean()
+
+    def imbalance_items(owned):
+        loads = np.array([cost[o].sum() for o in owned])
+        return loads.max() / loads.mean()
+
+    by_nnz = imbalance(nnz_balanced_ranges(ptr, 8))
+    by_cost = imbalance(cost_balanced_ranges(ptr, 8))
+    owned = dealt_assignment(ptr, 8)
+    dealt = imbalance_items(owned)
+    print(f"C5 W side, P=8: max/mean modelled rank time nnz-balanced {by_nnz:.3f}, "
+          f"cost-balanced ranges {by_cost:.3f}, dealt {dealt:.3f}")
+    assert by_cost < by_nnz
+    assert dealt <= 1.10
+    assert np.array_equal(np.sort(np.concatenate(owned)), np.arange(len(sizes)))
+
+
+def test_dealt_assignment_properties():
+    from paper_1604_04026_b200.plan import dealt_assignment, subproblem_cost
+
+    rng = np.random.default_rng(8)
+    for parts in (1, 2, 3, 8):
+        sizes = rng.zipf(1.2, size=3000).clip(max=3_000_000)
+        ptr = np.concatenate([[0], np.cumsum(sizes)])
+        owned = dealt_assignment(ptr, parts)
+        assert len(owned) == parts
+        allv = np.concatenate(owned)
+        assert np.array_equal(np.sort(allv), np.arange(len(sizes)))  # a partition
+        assert all(np.all(np.diff(o) > 0) for o in owned)  # ascending
+        c = subproblem_cost(sizes)
+        loads = np.array([c[o].sum() for o in owned])
+        assert loads.max() <= c.sum() / parts + c.max()
