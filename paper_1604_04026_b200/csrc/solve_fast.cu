@@ -39,6 +39,7 @@
 //       than a cluster: G CTAs per row, reductions through global memory.
 #include <cooperative_groups.h>
 
+#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
@@ -273,15 +274,57 @@ struct TReduce {
     }
 };
 
+// Checked build (build.py variant "checked", tools/checked_run.py): device-side
+// bounds checks and inter-CTA protocol assertions.  A violation is counted
+// (and its first code recorded) instead of trapping, so the run continues
+// and the host reads the counters after the workload (klnmf_debug_checks).
+// Codes: 1 gather offset, 2 item id, 3 maintained-product index, 4 moving
+// store, 5 product store, 6 cooperative slot overwritten before it was read
+// (parity reuse violated), 7 arrival counter two rounds ahead, 8 spill
+// record out of range, 9 non-finite / negative entry state, 10 cluster inbox
+// round mismatch.
+#ifdef KLNMF_CHECKED
+__device__ unsigned long long g_check[2];
+__device__ __forceinline__ void kcheck(bool ok, unsigned code) {
+    if (!ok) {
+        atomicAdd(&g_check[0], 1ull);
+        atomicCAS(&g_check[1], 0ull, (unsigned long long)code);
+    }
+}
+#else
+__device__ __forceinline__ void kcheck(bool, unsigned) {}
+#endif
+
+// index of an entry's maintained product in t_in (through the entry map)
+__device__ __forceinline__ int64_t t_index(const klnmf_solve_args_t &a, int64_t q) {
+    const int64_t i = a.tmap ? (int64_t)a.tmap[q] : q;
+    kcheck(i >= 0 && i < a.side.nnz, 3);
+    return i;
+}
+// gather offset (row * rp) of an entry's fixed-factor row
+__device__ __forceinline__ int gather_off(const klnmf_solve_args_t &a, int64_t q) {
+    const int32_t row = a.side.idx[q];
+    kcheck(row >= 0 && row < a.side.n_fix, 1);
+    return row * a.rp;
+}
+__device__ __forceinline__ int64_t item_at(const klnmf_solve_args_t &a, int64_t slot) {
+    const int64_t j = item_at(a, slot);
+    kcheck(j >= 0 && j < a.side.n_mov, 2);
+    return j;
+}
+
 // A result of this rank's subproblems (a moving-factor value, a maintained
 // product): stored locally and, in a fused sharded exchange, into every
 // peer's copy through its CUDA-IPC mapping (NVLink stores issued as the
 // results are produced) -- no all-gather follows the half-step.
 __device__ __forceinline__ void put_moving(const klnmf_solve_args_t &a, float *moving, int64_t i, float v) {
+    kcheck(i >= 0 && i < a.side.n_mov * a.rp, 4);
     moving[i] = v;
     for (int p = 0; p < a.n_peers; ++p) static_cast<float *>(a.peer_moving[p])[i] = v;
 }
 __device__ __forceinline__ void put_t(const klnmf_solve_args_t &a, int64_t i, double v) {
+    kcheck(i >= 0 && i < a.side.nnz, 5);
+    kcheck(v >= 0.0 && v < INFINITY, 9);
     a.t_out[i] = v;
     for (int p = 0; p < a.n_peers; ++p) a.peer_t[p][i] = v;
 }
@@ -353,7 +396,9 @@ struct PhaseClock {
 
 // ---------------------------------------------------------------------------
 // Warp kernel: groups of L <= 32 lanes, 32/L subproblems per warp in lock-step.
-template <int L, int NPL>
+// CTR: counter coordinate order (a compile-time switch, so the shared order's
+// code is not slowed by the per-subproblem order's indirections).
+template <int L, int NPL, bool CTR>
 __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_t a) {
     constexpr int NT = 128;
     constexpr int GPB = NT / L;  // groups per block
@@ -390,13 +435,13 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
     const float *fixed = static_cast<const float *>(a.fixed);
     float *moving = static_cast<float *>(a.moving);
     const float *val = static_cast<const float *>(a.side.val);
-    const int64_t j = valid ? (int64_t)a.items[slot] : 0;
+    const int64_t j = valid ? item_at(a, slot) : 0;
     const int64_t lo = valid ? a.side.ptr[j] : 0;
     const int s = valid ? (int)(a.side.ptr[j + 1] - lo) : 0;
 
     load_row(xs, moving + j * rp, pin, r, gl, L, valid);
     const int nchunks = (r + C - 1) / C;
-    const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
+    constexpr bool counter = CTR;
     uint8_t *cord = cord_all + grp * MAX_CHUNKS;
     if (counter && gl == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
     __syncwarp();
@@ -408,8 +453,8 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
         const int p = gl + e * L;
         if (p < s) {
             const int64_t q = lo + p;
-            roff[e] = a.side.idx[q] * rp;
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[q] : q], val[q], pm.eps_div, u[e], vi[e]);
+            roff[e] = gather_off(a, q);
+            entry_init(a.t_in[t_index(a, q)], val[q], pm.eps_div, u[e], vi[e]);
         } else {
             roff[e] = 0;
             u[e] = vi[e] = 0.0;  // contributes exactly 0 to every sum
@@ -469,8 +514,8 @@ __global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_
                 ph.count(8);
                 fresh = true;
             }
-            double x = live ? (double)xs[tt] : 0.0;
-            const double base = (live ? ssum[tt] : 0.0) + pm.beta;
+            double x = (!counter || live) ? (double)xs[tt] : 0.0;
+            const double base = ((!counter || live) ? ssum[tt] : 0.0) + pm.beta;
             double g = (base + pm.alpha * x) - tot[q];
             double h = pm.alpha + tot[C + q];
             int inner = 0;
@@ -565,7 +610,7 @@ struct BlockSums {
 };
 
 // One subproblem per block, NPL register entries per thread.
-template <int NT, int NPL>
+template <int NT, int NPL, bool CTR>
 __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_t a) {
     constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -585,7 +630,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     const float *fixed = static_cast<const float *>(a.fixed);
     float *moving = static_cast<float *>(a.moving);
     const float *val = static_cast<const float *>(a.side.val);
-    const int64_t j = a.items[slot];
+    const int64_t j = item_at(a, slot);
     const int64_t lo = a.side.ptr[j];
     const int s = (int)(a.side.ptr[j + 1] - lo);
 
@@ -599,8 +644,8 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
         const int p = tid + e * NT;
         if (p < s) {
             const int64_t q = lo + p;
-            roff[e] = a.side.idx[q] * rp;
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[q] : q], val[q], pm.eps_div, u[e], vi[e]);
+            roff[e] = gather_off(a, q);
+            entry_init(a.t_in[t_index(a, q)], val[q], pm.eps_div, u[e], vi[e]);
         } else {
             roff[e] = 0;
             u[e] = vi[e] = 0.0;
@@ -608,7 +653,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
     }
     const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
-    const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
+    constexpr bool counter = CTR;
     if (counter) {
         if (tid == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
         __syncthreads();
@@ -646,7 +691,7 @@ __global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_
         for (int cc = 0; cc < nc; ++cc) {
             const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
             const int tt = pc * C + q;
-            if (tt >= r) continue;  // counter order: padding slot of the last chunk
+            if (counter && tt >= r) continue;  // counter order: padding slot of the last chunk
             if (!fresh) {  // block-uniform
                 double red[NV];
 #pragma unroll
@@ -733,9 +778,13 @@ namespace cg = cooperative_groups;
 // rows, or of one row) share an SM, so one CTA's reduction and gather latency
 // overlaps the other's arithmetic.  16 resident entries per thread: 8 in
 // registers (u, 1/v, row offset), 8 in shared memory.
-constexpr int CL_NT = 256, CL_NR = 8, CL_NS = 8, CL_PER_SM = 2;
+#ifndef KLNMF_CL_NT  // slice-CTA shape (overridable for experiments)
+#define KLNMF_CL_NT 256
+#define KLNMF_CL_PER_SM 2
+#endif
+constexpr int CL_NT = KLNMF_CL_NT, CL_NR = 8, CL_NS = 8, CL_PER_SM = KLNMF_CL_PER_SM;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
-constexpr int CL_MAXG = 512;          // most CTAs in one cooperative row group
+constexpr int CL_MAXG = CL_PER_SM > 2 ? 1024 : 512;  // most CTAs in one cooperative row group
 constexpr size_t COOP_GROUP_BYTES = 2 * CL_MAXG * NV * 2 * sizeof(unsigned long long) + 128;
 
 // Per-entry record of the spilled entries of the long-row kernels (scratch).
@@ -810,8 +859,16 @@ __device__ __forceinline__ void st_async_v2(unsigned raddr, double x, double y, 
 
 constexpr int CL_MAXK = 16;  // largest cluster
 // Per-CTA inbox of the cluster all-reduce: round parity x source CTA x value.
+#ifdef KLNMF_CHECKED
+constexpr unsigned INBOX_TAG_BYTES = 16;  // checked build: (round, sender) rides along
+#else
+constexpr unsigned INBOX_TAG_BYTES = 0;
+#endif
 struct ClusterInbox {
     __align__(16) double box[2][CL_MAXK][NV];
+#ifdef KLNMF_CHECKED
+    __align__(16) double tag[2][CL_MAXK][2];
+#endif
     __align__(8) unsigned long long mbar[2];
 };
 
@@ -843,9 +900,18 @@ struct ClusterReducer {
                     const unsigned peer = (unsigned)(i / (NV / 2));
                     st_async_v2(mapa_u32(slot + 16u * q, peer), x0, x1, mapa_u32(mb, peer));
                 }
-                if (lane == 0) mbar_arrive_tx(mb, (unsigned)(k * NV * sizeof(double)));
+#ifdef KLNMF_CHECKED
+                if (lane < k)
+                    st_async_v2(mapa_u32(smem_u32(&P.tag[b][rank][0]), (unsigned)lane), (double)round, (double)rank,
+                                mapa_u32(mb, (unsigned)lane));
+#endif
+                if (lane == 0) mbar_arrive_tx(mb, (unsigned)(k * (NV * sizeof(double) + INBOX_TAG_BYTES)));
                 while (!mbar_try(mb, (round >> 1) & 1u)) {
                 }
+#ifdef KLNMF_CHECKED
+                // every peer's partial of this round, none of an older or newer one
+                if (lane < k) kcheck(P.tag[b][lane][0] == (double)round && P.tag[b][lane][1] == (double)lane, 10);
+#endif
                 if (lane < NV) {
                     double t = 0.0;
                     for (int c = 0; c < k; ++c) t += P.box[b][c][lane];
@@ -908,12 +974,15 @@ struct CoopReducer {
             if (lane == 0) {
                 atomicAdd(counter, 1u);
                 const unsigned target = (unsigned)G * (round + 1u);
-                while (*(volatile unsigned *)counter < target) __nanosleep(32);
+                unsigned seen;
+                while ((seen = *(volatile unsigned *)counter) < target) __nanosleep(32);
+                // no partner can arrive twice before this CTA arrives again
+                kcheck(seen <= (unsigned)G * (round + 2u), 7);
             }
         }
         __syncthreads();
-        if (w < NV) {
-            const unsigned long long *col = slots + ((size_t)b * NV + w) * CL_MAXG * 2;
+        for (int vw = w; vw < NV; vw += CL_NT / 32) {  // warp vw sums value vw (any CTA width)
+            const unsigned long long *col = slots + ((size_t)b * NV + vw) * CL_MAXG * 2;
             double acc = 0.0;
             for (int c0 = 0; c0 < G; c0 += 32) {
                 const int c = c0 + lane;
@@ -921,6 +990,8 @@ struct CoopReducer {
                 if (c < G) {
                     ulonglong2 q = ld_relaxed_v2(col + 2 * c);
                     while ((unsigned)q.x != (unsigned)tag || (unsigned)q.y != (unsigned)tag) {
+                        // a newer tag means round n+2 overwrote this slot before it was read
+                        kcheck((unsigned)q.x <= (unsigned)tag && (unsigned)q.y <= (unsigned)tag, 6);
                         __nanosleep(32);
                         q = ld_relaxed_v2(col + 2 * c);
                     }
@@ -929,7 +1000,7 @@ struct CoopReducer {
                 acc += x;
             }
             acc = warp_sum(acc);
-            if (lane == 0) R.tot[buf][w] = acc;
+            if (lane == 0) R.tot[buf][vw] = acc;
         }
         __syncthreads();
         ++round;
@@ -937,7 +1008,7 @@ struct CoopReducer {
 };
 
 // One subproblem's slice on one CTA (rank cq of the k CTAs sharing it).
-template <typename Reducer>
+template <bool CTR, typename Reducer>
 __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t slot, int cq, int k, Reducer &reduce,
                                             GroupRed &R, unsigned char *smem_raw, const double *ssum) {
     constexpr int NT = CL_NT, NR = CL_NR, NS = CL_NS;
@@ -955,7 +1026,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const float *fixed = static_cast<const float *>(a.fixed);
     float *moving = static_cast<float *>(a.moving);
     const float *val = static_cast<const float *>(a.side.val);
-    const int64_t j = a.items[slot];
+    const int64_t j = item_at(a, slot);
     const int64_t lo = a.side.ptr[j];
     const int64_t s = a.side.ptr[j + 1] - lo;
     const int64_t per = (s + k - 1) / k;
@@ -978,8 +1049,8 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         const int64_t i = tid + (int64_t)e * NT;
         if (i < cn) {
             const int64_t g = base + i;
-            off[e] = a.side.idx[g] * rp;
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, u[e], vi[e]);
+            off[e] = gather_off(a, g);
+            entry_init(a.t_in[t_index(a, g)], val[g], eps, u[e], vi[e]);
         } else {
             off[e] = -1;
             u[e] = vi[e] = 0.0;
@@ -992,8 +1063,8 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         const int si = e * NT + tid;
         if (i < cn) {
             const int64_t g = base + i;
-            offs[e] = a.side.idx[g] * rp;
-            entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, Us[si], VIs[si]);
+            offs[e] = gather_off(a, g);
+            entry_init(a.t_in[t_index(a, g)], val[g], eps, Us[si], VIs[si]);
         } else {
             offs[e] = -1;
             Us[si] = VIs[si] = 0.0;
@@ -1003,12 +1074,13 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const int64_t g = base + i;
         double2 uv;
-        entry_init(a.t_in[a.tmap ? (int64_t)a.tmap[g] : g], val[g], eps, uv.x, uv.y);
+        entry_init(a.t_in[t_index(a, g)], val[g], eps, uv.x, uv.y);
+        kcheck(base + i < a.side.nnz, 8);
         UVg[i].uv = uv;
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
-    const bool counter = a.order_mode != KLNMF_ORDER_SHARED;
+    constexpr bool counter = CTR;
     if (counter && tid == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
     __syncthreads();
     ph.mark(0);
@@ -1030,7 +1102,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         // (each thread stages and later reads only its own records)
 #pragma unroll 4
         for (int64_t i = spill0 + tid; i < cn; i += NT)
-            __stcg(&UVg[i].a, ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C));
+            __stcg(&UVg[i].a, ldg_f4(fixed + (int64_t)gather_off(a, base + i) + pc * C));
         cp_wait<0>();
         ph.mark(1);
         const float4 *A = cache + tid;
@@ -1042,7 +1114,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         for (int cc = 0; cc < nc; ++cc) {
             const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
             const int tt = pc * C + q;
-            if (tt >= r) continue;  // counter order: padding slot of the last chunk
+            if (counter && tt >= r) continue;  // counter order: padding slot of the last chunk
             if (!fresh) {  // uniform over the group
                 double red[NV];
 #pragma unroll
@@ -1159,6 +1231,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     ph.flush(std::is_same<Reducer, CoopReducer>::value ? 1 : 0, threadIdx.x == 0);
 }
 
+template <bool CTR>
 __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_cluster_kernel(const klnmf_solve_args_t a) {
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.num_blocks();
@@ -1178,7 +1251,7 @@ __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_cluster_kernel(const k
     if (k > 1) cl.sync();  // every inbox is initialised before the first push
     else __syncthreads();
     ClusterReducer red{R, P, k, cq, 0u};
-    solve_slice(a, slot, cq, k, red, R, smem_raw, ssum);
+    solve_slice<CTR>(a, slot, cq, k, red, R, smem_raw, ssum);
     if (k > 1) cl.sync();  // no CTA exits while a peer may still address it
 }
 
@@ -1188,6 +1261,7 @@ __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_cluster_kernel(const k
 // A row group's waits only point to rows of the same or an earlier wave and
 // every CTA is resident (cooperative launch), so the schedule cannot deadlock.
 
+template <bool CTR>
 __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_coop_kernel(const klnmf_solve_args_t a, const int4 *schedule,
                                                               int n_waves, unsigned char *sync) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1201,22 +1275,26 @@ __global__ void __launch_bounds__(CL_NT, CL_PER_SM) solve_coop_kernel(const klnm
         CoopReducer red{R, reinterpret_cast<unsigned long long *>(gb),
                         reinterpret_cast<unsigned *>(gb + COOP_GROUP_BYTES - 128), job.z, job.y, 0u};
         __syncthreads();  // shared buffers of the previous row are no longer read
-        solve_slice(a, job.x, job.y, job.z, red, R, smem_raw, ssum);
+        solve_slice<CTR>(a, job.x, job.y, job.z, red, R, smem_raw, ssum);
     }
 }
 
 struct FastKernel {
     int lanes, npl, nt;
     int64_t capacity;  // -1 = unbounded
-    void (*fn)(const klnmf_solve_args_t);
+    void (*fn)(const klnmf_solve_args_t);      // shared coordinate order
+    void (*fn_ctr)(const klnmf_solve_args_t);  // counter coordinate order
     int gpb;           // subproblems per block
     int ring_entries;  // float4 ring slots per thread and stage (NPL)
     int cluster;       // CTAs per subproblem (cluster kernel), 0 = plain launch, -1 = cooperative
 };
 
-#define WK(L, NPL) {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL>, 128 / (L), NPL, 0}
-#define BK(NT, NPL) {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL>, 1, NPL, 0}
-#define CK(K) {CL_NT * (K), CL_NE, CL_NT, (int64_t)(K) * CL_NT * CL_NE, solve_cluster_kernel, 1, 0, (K)}
+#define WK(L, NPL) \
+    {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL, false>, solve_warp_kernel<L, NPL, true>, 128 / (L), NPL, 0}
+#define BK(NT, NPL) \
+    {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL, false>, solve_block_kernel<NT, NPL, true>, 1, NPL, 0}
+#define CK(K) \
+    {CL_NT * (K), CL_NE, CL_NT, (int64_t)(K) * CL_NT * CL_NE, solve_cluster_kernel<false>, solve_cluster_kernel<true>, 1, 0, (K)}
 // Ascending capacity.  Every padding slot of a subproblem costs as much as a
 // real entry, so the ladder is dense (<= 25% steps) where the F side's and the
 // W side's subproblem sizes concentrate (SURVEY.md §8(d) size profiles).
@@ -1226,7 +1304,7 @@ const FastKernel kFast[] = {
     BK(64, 10), BK(64, 12), BK(64, 14), BK(64, 16), BK(128, 12), BK(128, 16), BK(256, 12), BK(256, 16),
     CK(2),      CK(4),      CK(8),      CK(16),
     // unbounded: the cooperative long-row kernel (klnmf_solve_coop, schedule built by the caller)
-    {CL_NT, CL_NE, CL_NT, -1, nullptr, 1, 0, -1},
+    {CL_NT, CL_NE, CL_NT, -1, nullptr, nullptr, 1, 0, -1},
 };
 #undef WK
 #undef BK
@@ -1240,6 +1318,18 @@ inline size_t slice_smem(int rp) {
 
 }  // namespace
 }  // namespace klnmf
+
+#ifdef KLNMF_CHECKED
+// checked build only: (violations, first violation code); optionally cleared
+extern "C" int klnmf_debug_checks(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, klnmf::g_check, sizeof(klnmf::g_check)) != cudaSuccess) return 1;
+    if (reset) {
+        static const unsigned long long zero[2] = {0, 0};
+        if (cudaMemcpyToSymbol(klnmf::g_check, zero, sizeof(zero)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+#endif
 
 #ifdef KLNMF_PHASE_TIMING
 // diagnostic build only: copies out (and optionally clears) the phase counters
@@ -1264,6 +1354,23 @@ extern "C" int klnmf_fast_kernel_count(void) { return kNumFast; }
 // shared memory (row sums, visit map, per-group sums) reaches ~11 KB.
 constexpr size_t SMEM_OPTIN = 32 * 1024;
 
+// cudaFuncAttributeNonPortableClusterSizeAllowed once per kernel function.
+static cudaError_t ensure_nonportable(const void *fn) {
+    static const void *done[8] = {};
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const void *d : done)
+        if (d == fn) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess)
+        for (auto &d : done)
+            if (!d) {
+                d = fn;
+                break;
+            }
+    return e;
+}
+
 static size_t fast_kernel_smem(const FastKernel &k, int32_t rp) {
     if (k.cluster != 0) return slice_smem(rp);
     return sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt +
@@ -1287,36 +1394,35 @@ extern "C" int klnmf_fast_kernel_info(int kernel_id, int64_t *capacity, int32_t 
     return 0;
 }
 
-static bool g_nonportable_set = false;
-
 // Sets every fp32 kernel's launch attributes (dynamic shared memory for the
-// larger, counter-order layout; non-portable cluster sizes) for padded rank
-// rp, so that later launches -- in particular inside CUDA-graph capture --
-// issue no attribute calls.
+// larger, counter-order layout; non-portable cluster sizes), both coordinate
+// orders, for padded rank rp, so that later launches -- in particular inside
+// CUDA-graph capture -- issue no attribute calls.
 extern "C" int klnmf_prepare_fast(int32_t rp) {
     if (rp % 4 != 0 || rp > KMAX_RP) return set_error_msg(1, "klnmf_prepare_fast: bad padded rank");
     cudaFuncAttributes fa;
-    KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)solve_coop_kernel));  // loads the module now
+    KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)solve_coop_kernel<false>));  // loads the module now
     int dev = 0, lim = 0;
     KLNMF_CHECK(cudaGetDevice(&dev));
     KLNMF_CHECK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     for (int id = 0; id < kNumFast; ++id) {
         const FastKernel &k = kFast[id];
         if (fast_kernel_smem(k, rp) + 8 * 1024 > (size_t)lim) continue;  // not used at this rank
-        if (k.fn) KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)k.fn));
         if (k.cluster < 0) {
-            KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, slice_smem(rp)));
-        } else if (k.cluster > 0) {
-            KLNMF_CHECK(ensure_smem((const void *)k.fn, slice_smem(rp)));
-            if (k.cluster > 8 && !g_nonportable_set) {
-                KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-                g_nonportable_set = true;
+            KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel<false>, slice_smem(rp)));
+            KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel<true>, slice_smem(rp)));
+            continue;
+        }
+        for (auto fn : {k.fn, k.fn_ctr}) {
+            KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)fn));
+            if (k.cluster > 0) {
+                KLNMF_CHECK(ensure_smem((const void *)fn, slice_smem(rp)));
+                if (k.cluster > 8)
+                    KLNMF_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            } else {
+                const size_t smem = fast_kernel_smem(k, rp);
+                if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)fn, smem));
             }
-        } else {
-            const size_t smem = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries *
-                                    (size_t)k.nt +
-                                2 * sizeof(float) * (size_t)k.gpb * (size_t)(rp | 1) + (size_t)k.gpb * MAX_CHUNKS + 16;
-            if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
         }
     }
     return 0;
@@ -1337,15 +1443,13 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
         return set_error_msg(1, "klnmf_solve_fast: n_peers > 0 needs both peer pointer arrays");
     const FastKernel &k = kFast[kernel_id];
     if (k.cluster < 0) return set_error_msg(1, "klnmf_solve_fast: the long-row bucket runs through klnmf_solve_coop");
+    void (*fn)(const klnmf_solve_args_t) = args->order_mode == KLNMF_ORDER_SHARED ? k.fn : k.fn_ctr;
     if (k.cluster > 0) {
         if (args->scratch == nullptr)
             return set_error_msg(1, "klnmf_solve_fast: the cluster kernel needs a scratch buffer");
         const size_t smem = slice_smem(args->rp);
-        KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
-        if (k.cluster > 8 && !g_nonportable_set) {
-            KLNMF_CHECK(cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            g_nonportable_set = true;
-        }
+        KLNMF_CHECK(ensure_smem((const void *)fn, smem));
+        if (k.cluster > 8) KLNMF_CHECK(ensure_nonportable((const void *)fn));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(args->n_items * k.cluster), 1, 1);
         cfg.blockDim = dim3((unsigned)k.nt, 1, 1);
@@ -1358,26 +1462,27 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        KLNMF_CHECK(cudaLaunchKernelEx(&cfg, k.fn, *args));
+        KLNMF_CHECK(cudaLaunchKernelEx(&cfg, fn, *args));
         return 0;
     }
     const int64_t blocks = (args->n_items + k.gpb - 1) / k.gpb;
     const size_t ring = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt;
     const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) +
                         (args->order_mode != KLNMF_ORDER_SHARED ? (size_t)k.gpb * MAX_CHUNKS : 0) + 16;
-    if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)k.fn, smem));
-    k.fn<<<(unsigned)blocks, k.nt, smem, as_stream(stream)>>>(*args);
+    if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)fn, smem));
+    fn<<<(unsigned)blocks, k.nt, smem, as_stream(stream)>>>(*args);
     KLNMF_CHECK_LAUNCH("klnmf_solve_fast");
     return 0;
 }
 
 extern "C" int klnmf_coop_info(int32_t rp, int64_t *entries_per_cta, int32_t *n_ctas, int64_t *sync_bytes_per_group) {
     const size_t smem = slice_smem(rp);
-    KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, smem));
+    KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel<false>, smem));
+    KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel<true>, smem));
     int dev = 0, sms = 0, per_sm = 0;
     KLNMF_CHECK(cudaGetDevice(&dev));
     KLNMF_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    KLNMF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_coop_kernel, CL_NT, smem));
+    KLNMF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_coop_kernel<false>, CL_NT, smem));
     *entries_per_cta = (int64_t)CL_NT * CL_NE;
     *n_ctas = sms * per_sm < CL_MAXG ? sms * per_sm : CL_MAXG;
     *sync_bytes_per_group = (int64_t)COOP_GROUP_BYTES;
@@ -1399,14 +1504,16 @@ extern "C" int klnmf_solve_coop(const klnmf_solve_args_t *args, const void *sche
         return set_error_msg(1, "klnmf_solve_coop: n_peers > 0 needs both peer pointer arrays");
     cudaStream_t st = as_stream(stream);
     const size_t smem = slice_smem(args->rp);
-    KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel, smem));
+    const void *fn = args->order_mode == KLNMF_ORDER_SHARED ? (const void *)solve_coop_kernel<false>
+                                                            : (const void *)solve_coop_kernel<true>;
+    KLNMF_CHECK(ensure_smem(fn, smem));
     KLNMF_CHECK(cudaMemsetAsync(sync, 0, (size_t)n_groups * COOP_GROUP_BYTES, st));  // tag 0: empty
     klnmf_solve_args_t a = *args;
     const int4 *sched = static_cast<const int4 *>(schedule);
     unsigned char *sy = static_cast<unsigned char *>(sync);
     int nw = n_waves;
     void *kargs[] = {&a, &sched, &nw, &sy};
-    KLNMF_CHECK(cudaLaunchCooperativeKernel((const void *)solve_coop_kernel, dim3((unsigned)n_ctas), dim3(CL_NT),
+    KLNMF_CHECK(cudaLaunchCooperativeKernel(fn, dim3((unsigned)n_ctas), dim3(CL_NT),
                                             kargs, smem, st));
     return 0;
 }

@@ -75,3 +75,17 @@ def test_cli_scaling_one_device(cuda_ok, tmp_path):
     assert rows[0] == ["r", "n_devices", "wall_seconds"]
     assert [(int(a), int(b)) for a, b, _ in rows[1:]] == [(4, 1), (8, 1)]
     assert all(float(c) > 0 for _, _, c in rows[1:])
+
+
+@pytest.mark.gpu
+def test_cli_scaling_torchrun_branch_two_ranks(cuda_ok, tmp_path):
+    """The P > 1 branch of `scaling`: torchrun launches one worker per rank,
+    each runs a sharded factorize, rank 0 writes the max-over-ranks wall
+    time.  On a one-GPU box the ranks share the device over gloo (the
+    launcher's test mode), so only the plumbing is exercised here."""
+    rc = cli.main(["scaling", "--config", "C1@m=300", "--r-values", "8", "--device-values", "1,2", "--iters", "2",
+                   "--precision", "fp32", "--backend", "gloo", "--out", str(tmp_path)])
+    assert rc == 0
+    rows = list(csv.reader(open(tmp_path / "scaling.csv")))
+    assert [(int(a), int(b)) for a, b, _ in rows[1:]] == [(8, 1), (8, 2)]
+    assert all(float(c) > 0 for _, _, c in rows[1:])

