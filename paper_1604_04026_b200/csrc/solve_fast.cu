@@ -308,7 +308,7 @@ __device__ __forceinline__ int gather_off(const klnmf_solve_args_t &a, int64_t q
     return row * a.rp;
 }
 __device__ __forceinline__ int64_t item_at(const klnmf_solve_args_t &a, int64_t slot) {
-    const int64_t j = item_at(a, slot);
+    const int64_t j = a.items[slot];
     kcheck(j >= 0 && j < a.side.n_mov, 2);
     return j;
 }
@@ -948,6 +948,13 @@ __device__ __forceinline__ void st_relaxed_v2(unsigned long long *p, unsigned lo
     asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
+#ifndef KLNMF_COOP_SLEEP_NS
+#define KLNMF_COOP_SLEEP_NS 32
+#endif
+__device__ __forceinline__ void coop_backoff() {
+    if (KLNMF_COOP_SLEEP_NS > 0) __nanosleep(KLNMF_COOP_SLEEP_NS);
+}
+
 struct CoopReducer {
     GroupRed &R;
     unsigned long long *slots;  // [2][NV][CL_MAXG][2] tagged words
@@ -975,7 +982,7 @@ struct CoopReducer {
                 atomicAdd(counter, 1u);
                 const unsigned target = (unsigned)G * (round + 1u);
                 unsigned seen;
-                while ((seen = *(volatile unsigned *)counter) < target) __nanosleep(32);
+                while ((seen = *(volatile unsigned *)counter) < target) coop_backoff();
                 // no partner can arrive twice before this CTA arrives again
                 kcheck(seen <= (unsigned)G * (round + 2u), 7);
             }
@@ -992,7 +999,7 @@ struct CoopReducer {
                     while ((unsigned)q.x != (unsigned)tag || (unsigned)q.y != (unsigned)tag) {
                         // a newer tag means round n+2 overwrote this slot before it was read
                         kcheck((unsigned)q.x <= (unsigned)tag && (unsigned)q.y <= (unsigned)tag, 6);
-                        __nanosleep(32);
+                        coop_backoff();
                         q = ld_relaxed_v2(col + 2 * c);
                     }
                     x = __longlong_as_double((long long)((q.x & 0xffffffff00000000ull) | (q.y >> 32)));

@@ -15,6 +15,12 @@ from paper_1604_04026_b200 import build as kb  # noqa: E402
 
 def main():
     name, defines = sys.argv[1], sys.argv[2:]
+    # "--src FILE": compile another solve_fast.cu (e.g. an older revision's)
+    src_fast = kb.CSRC / "solve_fast.cu"
+    if "--src" in defines:
+        i = defines.index("--src")
+        src_fast = Path(defines[i + 1]).resolve()
+        defines = defines[:i] + defines[i + 2:]
     out = REPO / "_variants" / name
     out.mkdir(parents=True, exist_ok=True)
     lib = kb.build()  # the regular objects are reused for every other file
@@ -22,8 +28,8 @@ def main():
     for src in kb.SOURCES:
         if src == "solve_fast.cu":
             o = out / "solve_fast.o"
-            subprocess.run([kb.nvcc(), *kb.ARCH, *kb.COMMON, *defines, "-c", str(kb.CSRC / src), "-o", str(o)],
-                           check=True)
+            subprocess.run([kb.nvcc(), *kb.ARCH, *kb.COMMON, "-I", str(kb.CSRC), *defines, "-c", str(src_fast),
+                            "-o", str(o)], check=True)
         else:
             o = kb.OBJDIR / (Path(src).stem + ".o")
         objs.append(str(o))
