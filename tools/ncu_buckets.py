@@ -1,7 +1,7 @@
 """Per-launch table (markdown) of an ncu report of all solver launches:
 duration, DRAM traffic and achieved GB/s, achieved occupancy, issue activity,
 FP64 pipe, shared-memory throughput and bank conflicts, top warp-stall
-reasons.  Usage: ncu_buckets.py REPORT"""
+reasons.  Usage: ncu_buckets.py REPORT|RAW_CSV"""
 import csv
 import io
 import re
@@ -17,7 +17,7 @@ COLS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "launch__registers_per_thread": "regs",
-    "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed": "smem",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "conf",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "wavef",
     "dram__bytes_read.sum": "dread",
@@ -37,7 +37,10 @@ def to_num(v, unit):
 
 
 def main(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # an exported raw page (ncu -i REP --page raw --csv)
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     ki = hdr.index("Kernel Name")
