@@ -398,8 +398,15 @@ struct PhaseClock {
 // Warp kernel: groups of L <= 32 lanes, 32/L subproblems per warp in lock-step.
 // CTR: counter coordinate order (a compile-time switch, so the shared order's
 // code is not slowed by the per-subproblem order's indirections).
+#ifndef KLNMF_WARP_MINB  // resident blocks per SM the warp kernels with NPL <= KLNMF_WARP_MINB_NPL
+#define KLNMF_WARP_MINB 1  // are compiled for (register cap; experiments)
+#endif
+#ifndef KLNMF_WARP_MINB_NPL
+#define KLNMF_WARP_MINB_NPL 14
+#endif
 template <int L, int NPL, bool CTR>
-__global__ void __launch_bounds__(128) solve_warp_kernel(const klnmf_solve_args_t a) {
+__global__ void __launch_bounds__(128, (NPL <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : 1))
+    solve_warp_kernel(const klnmf_solve_args_t a) {
     constexpr int NT = 128;
     constexpr int GPB = NT / L;  // groups per block
     constexpr int STAGES = ring_stages(NPL);
@@ -610,8 +617,12 @@ struct BlockSums {
 };
 
 // One subproblem per block, NPL register entries per thread.
+#ifndef KLNMF_BLOCK_MAXREG  // register cap of the block kernels (0 = none; experiments)
+#define KLNMF_BLOCK_MAXREG 0
+#endif
+constexpr int block_minb(int nt) { return KLNMF_BLOCK_MAXREG > 0 ? (65536 / (nt * KLNMF_BLOCK_MAXREG) > 0 ? 65536 / (nt * KLNMF_BLOCK_MAXREG) : 1) : 1; }
 template <int NT, int NPL, bool CTR>
-__global__ void __launch_bounds__(NT) solve_block_kernel(const klnmf_solve_args_t a) {
+__global__ void __launch_bounds__(NT, block_minb(NT)) solve_block_kernel(const klnmf_solve_args_t a) {
     constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);             // [STAGES][NPL][NT]
