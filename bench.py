@@ -11,9 +11,11 @@ Default workload: BASELINE.json config C4 (102,660 x 300,000, ~68M nnz,
 r=100, alpha1=alpha2=0.01, fp32 storage / fp64 arithmetic) -- the config the
 metric "outer iterations/sec and nnz*r coordinate updates/sec at 1/2/4/8
 B200" is specified on.  Synthetic data of that shape (synth.py), U(0,1)
-initial factors rounded to fp32.  Under torchrun (N>1) each rank owns an
-nnz-balanced range of subproblems per side and the updated factor rows are
-all-gathered over NCCL after each half-step (strong scaling: fixed C4).
+initial factors rounded to fp32.  Under torchrun (N>1) each rank owns a
+share of each side's subproblems balanced by modelled device time, and the
+solver kernels store their results into every peer's copy over NVLink
+(fused exchange; NCCL all-gather with KLNMF_FUSED_EXCHANGE=0), a barrier per
+half-step (strong scaling: fixed C4).
 
 value      nnz*r coordinate updates/s = 2*nnz*r / step time, data resident in HBM,
            device time (CUDA events, max over ranks), L2 flushed between steps.
@@ -540,7 +542,7 @@ def run_ours(args):
             "outer_iters_per_sec": 1e3 / ms_per_step,
             "config": {"workload": spec.name, "n": spec.n, "m": spec.m, "nnz": V.nnz, "rank": r,
                        "reg": vars(spec.reg), "precision": precision,
-                       "parallelism": f"dp{world} (nnz-balanced subproblem ranges; exchange: "
+                       "parallelism": f"dp{world} (subproblems split by modelled device time; exchange: "
                                       + ("fused peer stores over NVLink (CUDA IPC), NCCL barrier"
                                          if plan.fused_exchange else "NCCL all-gather" if world > 1 else "none")
                                       + ")",

@@ -398,15 +398,26 @@ struct PhaseClock {
 // Warp kernel: groups of L <= 32 lanes, 32/L subproblems per warp in lock-step.
 // CTR: counter coordinate order (a compile-time switch, so the shared order's
 // code is not slowed by the per-subproblem order's indirections).
-#ifndef KLNMF_WARP_MINB  // resident blocks per SM the warp kernels with NPL <= KLNMF_WARP_MINB_NPL
-#define KLNMF_WARP_MINB 1  // are compiled for (register cap; experiments)
+// Register caps (occupancy): the warp kernels with NPL <= 12 are compiled for
+// 4 resident blocks per SM (128 registers; the uncapped code used 164-165
+// and fit 3), the block kernels for <= 168 registers (the compiler's
+// 230-246 allowed 4 blocks of 64 threads, i.e. 8 warps per SM).  Measured
+// on C4: -9.5% per outer iteration; NPL = 14/16 keep their
+// registers (the shared-memory ring limits them to 3 blocks anyway).
+#ifndef KLNMF_WARP_MINB
+#define KLNMF_WARP_MINB 4
 #endif
 #ifndef KLNMF_WARP_MINB_NPL
-#define KLNMF_WARP_MINB_NPL 14
+#define KLNMF_WARP_MINB_NPL 12
 #endif
+#ifndef KLNMF_WARP_MINB_SMALL  // the same for NPL <= 7
+#define KLNMF_WARP_MINB_SMALL KLNMF_WARP_MINB
+#endif
+constexpr int warp_minb(int npl) {
+    return npl <= 7 ? KLNMF_WARP_MINB_SMALL : (npl <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : 1);
+}
 template <int L, int NPL, bool CTR>
-__global__ void __launch_bounds__(128, (NPL <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : 1))
-    solve_warp_kernel(const klnmf_solve_args_t a) {
+__global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const klnmf_solve_args_t a) {
     constexpr int NT = 128;
     constexpr int GPB = NT / L;  // groups per block
     constexpr int STAGES = ring_stages(NPL);
@@ -617,8 +628,8 @@ struct BlockSums {
 };
 
 // One subproblem per block, NPL register entries per thread.
-#ifndef KLNMF_BLOCK_MAXREG  // register cap of the block kernels (0 = none; experiments)
-#define KLNMF_BLOCK_MAXREG 0
+#ifndef KLNMF_BLOCK_MAXREG  // register cap of the block kernels (0 = none)
+#define KLNMF_BLOCK_MAXREG 168
 #endif
 constexpr int block_minb(int nt) { return KLNMF_BLOCK_MAXREG > 0 ? (65536 / (nt * KLNMF_BLOCK_MAXREG) > 0 ? 65536 / (nt * KLNMF_BLOCK_MAXREG) : 1) : 1; }
 template <int NT, int NPL, bool CTR>
@@ -1429,10 +1440,19 @@ extern "C" int klnmf_prepare_fast(int32_t rp) {
         if (k.cluster < 0) {
             KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel<false>, slice_smem(rp)));
             KLNMF_CHECK(ensure_smem((const void *)solve_coop_kernel<true>, slice_smem(rp)));
+#if defined(KLNMF_CARVEOUT) && KLNMF_CARVEOUT >= 0
+            KLNMF_CHECK(cudaFuncSetAttribute((const void *)solve_coop_kernel<false>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, KLNMF_CARVEOUT));
+            KLNMF_CHECK(cudaFuncSetAttribute((const void *)solve_coop_kernel<true>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, KLNMF_CARVEOUT));
+#endif
             continue;
         }
         for (auto fn : {k.fn, k.fn_ctr}) {
             KLNMF_CHECK(cudaFuncGetAttributes(&fa, (const void *)fn));
+#if defined(KLNMF_CARVEOUT) && KLNMF_CARVEOUT >= 0
+            KLNMF_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, KLNMF_CARVEOUT));
+#endif
             if (k.cluster > 0) {
                 KLNMF_CHECK(ensure_smem((const void *)fn, slice_smem(rp)));
                 if (k.cluster > 8)

@@ -17,12 +17,15 @@ Precision modes:
           maintained products carried between half-steps (klnmf_solve_fast).
 
 Multi-GPU (torch.distributed, one process per GPU): every rank holds V and
-both factors in full; subproblems are split into contiguous nnz-balanced
-ranges (columns for the F-update, rows for the W-update).  In fp32 mode the
-solver kernels store every result into all ranks' copies through CUDA-IPC
-mappings (the fused exchange, a barrier before and after each half-step);
-otherwise, after each half-step, the updated factor rows are all-gathered
-over NCCL.  Results are bitwise independent of the rank count: each
+both factors in full; the subproblems of each side (columns for the
+F-update, rows for the W-update) are split by a measured device-time model
+(``subproblem_cost``): with the fused exchange (fp32 default) the long rows
+are dealt across ranks and the rest cut into runs (``dealt_assignment``),
+otherwise contiguous cost-balanced ranges (fp32) or nnz-balanced ranges
+(fp64).  In fp32 mode the solver kernels store every result into all ranks'
+copies through CUDA-IPC mappings (the fused exchange, a barrier before and
+after each half-step); otherwise, after each half-step, the updated factor
+rows are all-gathered over NCCL.  Results are bitwise independent of the rank count: each
 subproblem is solved by exactly one rank with identical inputs, and row sums
 are computed from the full replica.
 
