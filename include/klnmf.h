@@ -262,7 +262,7 @@ int klnmf_coo_to_csc(const int32_t *rows, const int32_t *cols, const void *vals,
 
 /* nnz bucketing of subproblems j in [j_lo, j_hi): items sorted by nnz descending;
  * bucket_start[b] = first slot of bucket b where bucket b holds nnz <= bounds[b]
- * (bounds ascending, last bound may be INT64_MAX).  n_bounds <= 32. */
+ * (bounds ascending, last bound may be INT64_MAX).  n_bounds <= 64. */
 int klnmf_bucketize(const int64_t *ptr, int64_t j_lo, int64_t j_hi, const int64_t *bounds,
                     int n_bounds, int32_t *items, int64_t *bucket_count_host, void *stream);
 

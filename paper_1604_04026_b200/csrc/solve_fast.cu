@@ -155,6 +155,9 @@ __device__ __forceinline__ void entry_update(double delta, double a, double eps,
     const double q = fma(p, delta * a, 1.0);  // (t'+eps)/(t+eps)
     double un = u * fast_rcp(q);
     if (CLAMP && q < eps * p) un = fast_rcp(vi * eps);
+#ifdef KLNMF_EXP_MOVEDP  // experiment: +4 DP ops per entry update, results unchanged
+    un = (un + 0.0 * q) + 0.0 * p;
+#endif
     u = un;
 }
 
@@ -171,6 +174,9 @@ __device__ __forceinline__ void with_clamp(bool any_negative, F &&f) {
 __device__ __forceinline__ void accum(double &g, double &h, double u, double z, double av) {
     g = fma(u, av, g);
     h = fma(z * av, av, h);
+#ifdef KLNMF_EXP_PASSDP  // experiment: +2 DP ops per term, results unchanged (g finite)
+    h = h + 0.0 * g;
+#endif
 }
 
 // Partials of the chunk's coordinates CC..C-1 from one entry's 16-byte chunk
@@ -219,7 +225,7 @@ __device__ __forceinline__ float comp(const float4 *p, int c) { return reinterpr
 // before their stores, so a subproblem's start costs one load latency, not
 // one per position.
 __device__ __forceinline__ void load_row(float *xs, const float *row, const int *pin, int r, int first, int step,
-                                         bool valid) {
+                                         bool valid, float *xo = nullptr) {
     for (int k0 = first; k0 < r; k0 += 4 * step) {
         float v[4];
 #pragma unroll
@@ -229,7 +235,10 @@ __device__ __forceinline__ void load_row(float *xs, const float *row, const int 
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (k0 + i * step < r) xs[k0 + i * step] = v[i];
+            if (k0 + i * step < r) {
+                xs[k0 + i * step] = v[i];
+                if (xo) xo[k0 + i * step] = v[i];
+            }
     }
 }
 
@@ -400,9 +409,11 @@ struct PhaseClock {
 // code is not slowed by the per-subproblem order's indirections).
 // Register caps (occupancy): the warp kernels with NPL <= 12 are compiled for
 // 4 resident blocks per SM (128 registers; the uncapped code used 164-165
-// and fit 3), the block kernels for <= 168 registers (the compiler's
-// 230-246 allowed 4 blocks of 64 threads, i.e. 8 warps per SM).  Measured
-// on C4: -9.5% per outer iteration; NPL = 14/16 keep their
+// and fit 3), the block kernels for <= 128 registers at NPL <= 12 (16 warps
+// per SM; BK(256, *) had 8) and <= 168 above (the compiler's 230-246
+// allowed 8 warps per SM).  Measured on C4: the warp and
+// NPL > 12 block caps -9.2% per outer iteration against no caps, the
+// NPL <= 12 block cap a further -1.5%; NPL = 14/16 warp kernels keep their
 // registers (the shared-memory ring limits them to 3 blocks anyway).
 #ifndef KLNMF_WARP_MINB
 #define KLNMF_WARP_MINB 4
@@ -412,6 +423,9 @@ struct PhaseClock {
 #endif
 #ifndef KLNMF_WARP_MINB_SMALL  // the same for NPL <= 7
 #define KLNMF_WARP_MINB_SMALL KLNMF_WARP_MINB
+#endif
+#ifndef KLNMF_BATCH_TESTS  // batched entry tests after each chunk pass (warp kernels, L >= 4)
+#define KLNMF_BATCH_TESTS 1
 #endif
 constexpr int warp_minb(int npl) {
     return npl <= 7 ? KLNMF_WARP_MINB_SMALL : (npl <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : 1);
@@ -457,7 +471,10 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
     const int64_t lo = valid ? a.side.ptr[j] : 0;
     const int s = valid ? (int)(a.side.ptr[j + 1] - lo) : 0;
 
-    load_row(xs, moving + j * rp, pin, r, gl, L, valid);
+    // batched entry tests (L >= 4): the result row starts as the input row and
+    // only coordinates that enter the Newton loop write it
+    constexpr bool BATCH = KLNMF_BATCH_TESTS && L >= 4;
+    load_row(xs, moving + j * rp, pin, r, gl, L, valid, BATCH ? xo : nullptr);
     const int nchunks = (r + C - 1) / C;
     constexpr bool counter = CTR;
     uint8_t *cord = cord_all + grp * MAX_CHUNKS;
@@ -508,12 +525,14 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
         const uint32_t perm = counter ? chunk_perm4(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, ch)
                                       : PERM4_IDENTITY;
         bool fresh = false;  // tot valid for the current t
+        unsigned emask = 0;  // BATCH: slots of this chunk whose coordinate enters (valid while fresh)
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
             const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
             const int tt = pc * C + q;
             const bool live = tt < r;
-            if (__any_sync(FULL_MASK, !fresh)) {
+            const bool need_pass = __any_sync(FULL_MASK, !fresh);
+            if (need_pass) {
                 double red[NV];
 #pragma unroll
                 for (int i = 0; i < NV; ++i) red[i] = 0.0;
@@ -531,6 +550,28 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
                 ph.mark(3);
                 ph.count(8);
                 fresh = true;
+            }
+            if (BATCH) {
+                if (need_pass) {
+                    // entry tests of the slots cc..nc-1 at once, lane gl testing slot
+                    // cc + gl, with the same expressions as the visit below (so the
+                    // same bits): the visits no group enters are skipped
+                    const int sl = cc + gl;
+                    bool ent = false;
+                    if (valid && sl < nc) {
+                        const int qs = (int)((perm >> (2 * sl)) & 3u);
+                        const int ts = pc * C + qs;
+                        if (!counter || ts < r) {
+                            const double xv = (double)xs[ts];
+                            const double bv = ssum[ts] + pm.beta;
+                            ent = enters((bv + pm.alpha * xv) - tot[qs], xv, pm.eps_grad);
+                        }
+                    }
+                    const unsigned b = __ballot_sync(FULL_MASK, ent);
+                    const unsigned gb = L == 32 ? b : (b >> ((threadIdx.x & 31) & ~(L - 1))) & ((1u << (L & 31)) - 1u);
+                    emask = (gb & 0xFu) << cc;
+                }
+                if (!__any_sync(FULL_MASK, (emask >> cc) & 1u)) continue;  // x unchanged, xo = xs already
             }
             double x = (!counter || live) ? (double)xs[tt] : 0.0;
             const double base = ((!counter || live) ? ssum[tt] : 0.0) + pm.beta;
@@ -631,9 +672,18 @@ struct BlockSums {
 #ifndef KLNMF_BLOCK_MAXREG  // register cap of the block kernels (0 = none)
 #define KLNMF_BLOCK_MAXREG 168
 #endif
-constexpr int block_minb(int nt) { return KLNMF_BLOCK_MAXREG > 0 ? (65536 / (nt * KLNMF_BLOCK_MAXREG) > 0 ? 65536 / (nt * KLNMF_BLOCK_MAXREG) : 1) : 1; }
+#ifndef KLNMF_BLOCK_MAXREG_SMALL  // the same for NPL <= KLNMF_BLOCK_SMALL_NPL
+#define KLNMF_BLOCK_MAXREG_SMALL 128
+#endif
+#ifndef KLNMF_BLOCK_SMALL_NPL
+#define KLNMF_BLOCK_SMALL_NPL 12
+#endif
+constexpr int block_minb(int nt, int npl) {
+    const int cap = npl <= KLNMF_BLOCK_SMALL_NPL ? KLNMF_BLOCK_MAXREG_SMALL : KLNMF_BLOCK_MAXREG;
+    return cap > 0 ? (65536 / (nt * cap) > 0 ? 65536 / (nt * cap) : 1) : 1;
+}
 template <int NT, int NPL, bool CTR>
-__global__ void __launch_bounds__(NT, block_minb(NT)) solve_block_kernel(const klnmf_solve_args_t a) {
+__global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(const klnmf_solve_args_t a) {
     constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);             // [STAGES][NPL][NT]
@@ -1062,6 +1112,12 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const int64_t c0 = min(s, (int64_t)cq * per);
     const int64_t cn = min(s, c0 + per) - c0;  // entries of this CTA
     const int64_t base = lo + c0;              // global entry index of local entry 0
+    // resident entry slots in use (CTA-uniform): slots e >= ne hold no entry
+    // in any thread and are skipped, so a slice filled to 70% of its 16
+    // slots per thread costs ~70% of a full one
+    // (cooperative rows fill their slices by construction: no test there)
+    const int ne = std::is_same<Reducer, CoopReducer>::value ? NR + NS
+                                                             : (int)min((cn + NT - 1) / NT, (int64_t)(NR + NS));
     const double eps = pm.eps_div;
     // spilled entries (rows longer than the on-chip capacity of their CTAs):
     // one 32-byte record per entry in scratch -- (u, vi) and the current
@@ -1122,10 +1178,11 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         // gather this chunk of every resident entry once (own slots only)
 #pragma unroll
         for (int e = 0; e < NR; ++e)
-            cp_async16(cache_s + 16u * NT * e, fixed + max(off[e], 0) + pc * C, off[e] >= 0);
+            if (e < ne) cp_async16(cache_s + 16u * NT * e, fixed + max(off[e], 0) + pc * C, off[e] >= 0);
 #pragma unroll
         for (int e = 0; e < NS; ++e)
-            cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + pc * C, offs[e] >= 0);
+            if (NR + e < ne)
+                cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + pc * C, offs[e] >= 0);
         cp_commit();
         // spilled entries: stage the chunk's slice next to their state
         // (each thread stages and later reads only its own records)
@@ -1151,9 +1208,11 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                 with_cc(counter ? 0 : cc, [&](auto ccv) {
                     constexpr int CC = decltype(ccv)::value;
 #pragma unroll
-                    for (int e = 0; e < NR; ++e) accum_from<CC>(red, A[e * NT], u[e], entry_z(u[e], vi[e]));
+                    for (int e = 0; e < NR; ++e)
+                        if (e < ne) accum_from<CC>(red, A[e * NT], u[e], entry_z(u[e], vi[e]));
 #pragma unroll
                     for (int e = 0; e < NS; ++e) {
+                        if (NR + e >= ne) break;
                         const double uu = Us[e * NT + tid];
                         accum_from<CC>(red, A[(NR + e) * NT], uu, entry_z(uu, VIs[e * NT + tid]));
                     }
@@ -1191,12 +1250,14 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                         constexpr bool CL = decltype(cl)::value;
 #pragma unroll
                         for (int e = 0; e < NR; ++e) {  // register entries: branch-free
+                            if (e >= ne) break;
                             const double av = widen(comp(A + e * NT, q));
                             if (upd) entry_update<CL>(delta, av, eps, u[e], vi[e]);
                             if (again) accum(g2, h2, u[e], entry_z(u[e], vi[e]), av);
                         }
 #pragma unroll
                         for (int e = 0; e < NS; ++e) {
+                            if (NR + e >= ne) break;
                             const int si = e * NT + tid;
                             const double av = widen(comp(A + (NR + e) * NT, q));
                             double uu = Us[si];
@@ -1330,8 +1391,13 @@ struct FastKernel {
 const FastKernel kFast[] = {
     WK(1, 4),   WK(2, 4),   WK(4, 4),   WK(8, 4),   WK(8, 6),   WK(8, 8),   WK(16, 6),  WK(16, 8),
     WK(32, 5),  WK(32, 6),  WK(32, 7),  WK(32, 8),  WK(32, 10), WK(32, 12), WK(32, 14), WK(32, 16),
-    BK(64, 10), BK(64, 12), BK(64, 14), BK(64, 16), BK(128, 12), BK(128, 16), BK(256, 12), BK(256, 16),
-    CK(2),      CK(4),      CK(8),      CK(16),
+    BK(64, 10), BK(64, 12), BK(64, 14), BK(64, 16), BK(128, 10), BK(128, 12), BK(128, 14), BK(128, 16),
+    BK(256, 10), BK(256, 12), BK(256, 14), BK(256, 16),
+    // clusters of every width up to 8, then steps of 2: the W side's long
+    // rows spread evenly over (4096, 65536], and a cluster bucket spanning a
+    // factor of 2 left 30% of its slots empty
+    CK(2),      CK(3),      CK(4),      CK(5),      CK(6),      CK(7),      CK(8),      CK(10),
+    CK(12),     CK(14),     CK(16),
     // unbounded: the cooperative long-row kernel (klnmf_solve_coop, schedule built by the caller)
     {CL_NT, CL_NE, CL_NT, -1, nullptr, nullptr, 1, 0, -1},
 };

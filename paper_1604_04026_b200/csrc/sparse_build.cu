@@ -100,6 +100,8 @@ __global__ void bucket_counts(const int64_t *sorted_sizes, int64_t n, const int6
     }
 }
 
+constexpr int KMAX_BUCKETS = 64;  // size buckets of one side (the fp32 kernel ladder)
+
 inline unsigned grid_for(int64_t total, int nt) {
     int64_t b = (total + nt - 1) / nt;
     if (b < 1) b = 1;
@@ -224,7 +226,8 @@ extern "C" int klnmf_bucketize(const int64_t *ptr, int64_t j_lo, int64_t j_hi, c
                                int32_t *items, int64_t *bucket_count_host, void *stream) {
     cudaStream_t st = as_stream(stream);
     const int64_t n = j_hi - j_lo;
-    if (n_bounds < 1 || n_bounds > 32) return set_error_msg(1, "klnmf_bucketize: 1 <= n_bounds <= 32");
+    if (n_bounds < 1 || n_bounds > KMAX_BUCKETS)
+        return set_error_msg(1, "klnmf_bucketize: 1 <= n_bounds <= 64");
     if (n <= 0) {
         for (int b = 0; b < n_bounds; ++b) bucket_count_host[b] = 0;
         return 0;
@@ -235,8 +238,8 @@ extern "C" int klnmf_bucketize(const int64_t *ptr, int64_t j_lo, int64_t j_hi, c
     KLNMF_CHECK(cudaMallocAsync(&sizes, sizeof(int64_t) * (size_t)n, st));
     KLNMF_CHECK(cudaMallocAsync(&sizes_sorted, sizeof(int64_t) * (size_t)n, st));
     KLNMF_CHECK(cudaMallocAsync(&ids, sizeof(int32_t) * (size_t)n, st));
-    KLNMF_CHECK(cudaMallocAsync(&dbounds, sizeof(int64_t) * 64, st));
-    dcounts = dbounds + 32;
+    KLNMF_CHECK(cudaMallocAsync(&dbounds, sizeof(int64_t) * 2 * KMAX_BUCKETS, st));
+    dcounts = dbounds + KMAX_BUCKETS;
     KLNMF_CHECK(cudaMemcpyAsync(dbounds, bounds, sizeof(int64_t) * (size_t)n_bounds, cudaMemcpyHostToDevice, st));
     segment_sizes<<<grid_for(n, 256), 256, 0, st>>>(ptr, j_lo, n, sizes, ids);
     KLNMF_CHECK_LAUNCH("segment_sizes");

@@ -530,6 +530,9 @@ class DevicePlan:
         if count == 0:
             return
         per_cta, n_ctas, group_bytes = _lib.coop_info(self.rp)
+        lim = int(os.environ.get("KLNMF_COOP_CTAS", "0"))  # experiment knob: fewer CTAs than resident slots
+        if lim > 0:
+            n_ctas = min(n_ctas, lim)
         rows = sp.items[start:start + count].cpu().numpy()
         sizes = np.diff(sp.ptr_host)[rows]
         waves = []  # [free CTAs, list of (slot, c0, G)]
@@ -821,11 +824,16 @@ class DevicePlan:
         main = self.stream_ptr
         buckets = [b for b in side.buckets if b[2] > 0]
         coop_kid = self._stream_kernel_id()
-        # the cooperative long-row kernel first and alone (it wants every SM);
-        # the other buckets are independent (disjoint outputs, atomic stats)
-        # and fork over several streams, so one bucket's last partial wave and
-        # the few-subproblem buckets overlap the others
+        # the buckets are independent (disjoint outputs, atomic stats) and
+        # fork over several streams, so one bucket's last partial wave and
+        # the few-subproblem buckets overlap the others;
+        # the cooperative long-row kernel is launched first (largest bucket);
+        # it runs alongside the other buckets (their blocks fill the SM slots
+        # its waves leave free: -0.5 ms per C4 iteration), or alone before
+        # them with KLNMF_COOP_CONCURRENT=0
         first = [b for b in buckets if self.fp32 and b[0] == coop_kid]
+        if os.environ.get("KLNMF_COOP_CONCURRENT", "1") == "1":
+            first = []
         rest = [b for b in buckets if b not in first]
         n_par = min(len(self._par_streams), len(rest)) if (self.fp32 and self.concurrent) else 0
         for q, (kid, start, count) in enumerate(first + rest):
