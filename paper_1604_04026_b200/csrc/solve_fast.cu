@@ -427,8 +427,11 @@ struct PhaseClock {
 #ifndef KLNMF_BATCH_TESTS  // batched entry tests after each chunk pass (warp kernels, L >= 4)
 #define KLNMF_BATCH_TESTS 1
 #endif
+#ifndef KLNMF_WARP_MINB_LARGE  // the same for NPL > KLNMF_WARP_MINB_NPL
+#define KLNMF_WARP_MINB_LARGE 1
+#endif
 constexpr int warp_minb(int npl) {
-    return npl <= 7 ? KLNMF_WARP_MINB_SMALL : (npl <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : 1);
+    return npl <= 7 ? KLNMF_WARP_MINB_SMALL : (npl <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : KLNMF_WARP_MINB_LARGE);
 }
 template <int L, int NPL, bool CTR>
 __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const klnmf_solve_args_t a) {

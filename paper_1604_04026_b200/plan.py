@@ -339,7 +339,7 @@ class DevicePlan:
             # concurrently; concurrent = False launches them one at a time
             # (per-kernel timing without overlap)
             self.concurrent = True
-            self._par_streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("KLNMF_PAR_STREAMS", "4")))]
+            self._par_streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("KLNMF_PAR_STREAMS", "6")))]
             self._fork_event = self._new_event()
             self._join_events = [self._new_event() for _ in self._par_streams]
             if self.fp32:
