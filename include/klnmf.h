@@ -52,6 +52,9 @@ extern "C" {
 #define KLNMF_STATS_LEN 4
 
 int klnmf_abi_version(void);
+/* sizeof(klnmf_solve_args_t) / sizeof(klnmf_side_t) as compiled (binding checks) */
+int klnmf_sizeof_solve_args(void);
+int klnmf_sizeof_side(void);
 const char *klnmf_last_error(void);
 /* Counter-mode chunk order of one subproblem, computed on the host with the
  * device's generator (uint8 order[nchunks], nchunks <= 64). */
@@ -152,9 +155,9 @@ typedef struct {
     const int32_t *items;     /* subproblem (moving item) ids to solve */
     int64_t n_items;
     /* fp32 mode: maintained products carried between half-steps */
-    const int32_t *tmap;      /* nnz: index into t_in of each entry (NULL = identity) */
-    const double *t_in;
-    double *t_out;            /* nnz, entry order of this side */
+    const int32_t *tmap;      /* nnz: position of each entry in the other side's entry order */
+    const double *t_in;       /* nnz (see t_scatter) */
+    double *t_out;            /* nnz (see t_scatter) */
     double *scratch;          /* exact mode: nnz doubles; fp32 long-row kernels: 4*nnz (a 32-byte
                                  record per entry, used only by entries beyond the on-chip capacity) */
     int32_t r;
@@ -188,6 +191,12 @@ typedef struct {
     int32_t n_peers;
     void *const *peer_moving;
     double *const *peer_t;
+    /* fp32 mode, layout of the maintained products: 0 = t_in is read through
+     * tmap (other side's entry order) and t_out / peer_t written in this
+     * side's entry order; 1 = t_in is read in this side's entry order and
+     * t_out / peer_t written through tmap into the other side's entry order
+     * (coalesced reads at every subproblem start; scattered stores). */
+    int32_t t_scatter;
 } klnmf_solve_args_t;
 
 #define KLNMF_ORDER_SHARED 0
@@ -283,6 +292,11 @@ int klnmf_kl_data_term_dev(const klnmf_side_t *csc, const void *w, const void *f
  * instead of nnz r-dots.  Deterministic.  Result (fp64) in *out_host. */
 int klnmf_kl_data_term_t(const float *val, const double *t, int64_t nnz, double eps_div, double *out_host,
                          void *stream);
+/* the same with the products of entry q at t[tmap[q]] (stored in the other
+ * orientation; NULL = identity), summed in val's entry order -- so the value
+ * does not depend on which orientation the products are carried in */
+int klnmf_kl_data_term_t_mapped(const float *val, const double *t, const int32_t *tmap, int64_t nnz,
+                                double eps_div, double *out_host, void *stream);
 
 /* factor statistics over the r real columns: out_host[0] = sum x^2, [1] = sum x,
  * [2] = number of exact zeros (as double).  Deterministic. */

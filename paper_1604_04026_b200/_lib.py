@@ -24,6 +24,8 @@ INT = ctypes.c_int
 # Every symbol include/klnmf.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "klnmf_abi_version",
+    "klnmf_sizeof_solve_args",
+    "klnmf_sizeof_side",
     "klnmf_last_error",
     "klnmf_event_record",
     "klnmf_event_create",
@@ -61,6 +63,7 @@ EXPORTS = (
     "klnmf_init_t",
     "klnmf_kl_data_term_dev",
     "klnmf_kl_data_term_t",
+    "klnmf_kl_data_term_t_mapped",
     "klnmf_factor_stats",
     "klnmf_upload_i64_as_i32",
     "klnmf_upload_f64_as_f32",
@@ -126,11 +129,14 @@ class SolveArgs(ctypes.Structure):
         ("n_peers", I32),
         ("peer_moving", P),
         ("peer_t", P),
+        ("t_scatter", I32),
     ]
 
 
 _SIGS = {
     "klnmf_abi_version": ([], INT),
+    "klnmf_sizeof_solve_args": ([], INT),
+    "klnmf_sizeof_side": ([], INT),
     "klnmf_last_error": ([], ctypes.c_char_p),
     "klnmf_event_record": ([P, P, INT], INT),
     "klnmf_event_create": ([ctypes.POINTER(P)], INT),
@@ -168,6 +174,7 @@ _SIGS = {
     "klnmf_init_t": ([ctypes.POINTER(Side), P, P, I32, P, P, I32, P, P], INT),
     "klnmf_kl_data_term_dev": ([ctypes.POINTER(Side), P, P, I32, P, P, I32, INT, D, P, P], INT),
     "klnmf_kl_data_term_t": ([P, P, I64, D, P, P], INT),
+    "klnmf_kl_data_term_t_mapped": ([P, P, P, I64, D, P, P], INT),
     "klnmf_factor_stats": ([P, I64, I32, I32, INT, P, P], INT),
     "klnmf_upload_i64_as_i32": ([P, I64, P, P], INT),
     "klnmf_upload_f64_as_f32": ([P, I64, P, P], INT),

@@ -117,6 +117,8 @@ cudaError_t copy_columns(double *dst, const double *src, int64_t r, int64_t n, i
 using namespace klnmf;
 
 extern "C" int klnmf_abi_version(void) { return KLNMF_ABI_VERSION; }
+extern "C" int klnmf_sizeof_solve_args(void) { return (int)sizeof(klnmf_solve_args_t); }
+extern "C" int klnmf_sizeof_side(void) { return (int)sizeof(klnmf_side_t); }
 
 extern "C" const char *klnmf_last_error(void) { return g_err; }
 

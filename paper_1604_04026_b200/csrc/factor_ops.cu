@@ -213,14 +213,18 @@ extern "C" int klnmf_factor_stats(const void *fac, int64_t n_items, int32_t rp, 
 // block sums a fixed contiguous range in a fixed tree, then one warp sums the
 // block partials in order -- deterministic for a given nnz.
 constexpr int KL_BLOCKS = 1184, KL_NT = 256;  // 8 x 148 SMs
-__global__ void kl_t_partial(const float *val, const double *t, int64_t nnz, double eps, double *partial) {
+// tmap (may be NULL): t of entry q is t[tmap[q]] -- the products stored in
+// the other orientation, summed in val's (canonical) entry order
+__global__ void kl_t_partial(const float *val, const double *t, const int32_t *tmap, int64_t nnz, double eps,
+                             double *partial) {
     __shared__ double sh[KL_NT / 32];
     const int64_t per = (nnz + KL_BLOCKS - 1) / KL_BLOCKS;
     const int64_t lo = (int64_t)blockIdx.x * per, hi = min(nnz, lo + per);
     double s = 0.0;
     for (int64_t q = lo + threadIdx.x; q < hi; q += KL_NT) {
         const double v = (double)val[q];
-        s += v * log(v / (t[q] + eps)) - v;  // _kernels.py:158
+        const double tq = tmap ? t[tmap[q]] : t[q];
+        s += v * log(v / (tq + eps)) - v;  // _kernels.py:158
     }
     const double b = block_sum_det<KL_NT>(s, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = b;
@@ -235,11 +239,16 @@ __global__ void kl_t_final(const double *partial, double *out) {
 
 extern "C" int klnmf_kl_data_term_t(const float *val, const double *t, int64_t nnz, double eps_div,
                                     double *out_host, void *stream) {
+    return klnmf_kl_data_term_t_mapped(val, t, nullptr, nnz, eps_div, out_host, stream);
+}
+
+extern "C" int klnmf_kl_data_term_t_mapped(const float *val, const double *t, const int32_t *tmap, int64_t nnz,
+                                           double eps_div, double *out_host, void *stream) {
     cudaStream_t st = as_stream(stream);
     double *partial = nullptr;
     KLNMF_CHECK(keep_async_pool());
     KLNMF_CHECK(cudaMallocAsync(&partial, sizeof(double) * (KL_BLOCKS + 1), st));
-    kl_t_partial<<<KL_BLOCKS, KL_NT, 0, st>>>(val, t, nnz, eps_div, partial);
+    kl_t_partial<<<KL_BLOCKS, KL_NT, 0, st>>>(val, t, tmap, nnz, eps_div, partial);
     KLNMF_CHECK_LAUNCH("kl_t_partial");
     kl_t_final<<<1, 32, 0, st>>>(partial, partial + KL_BLOCKS);
     KLNMF_CHECK_LAUNCH("kl_t_final");

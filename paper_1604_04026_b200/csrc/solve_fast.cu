@@ -304,9 +304,11 @@ __device__ __forceinline__ void kcheck(bool ok, unsigned code) {
 __device__ __forceinline__ void kcheck(bool, unsigned) {}
 #endif
 
-// index of an entry's maintained product in t_in (through the entry map)
+// index of an entry's maintained product in t_in: the entry itself when the
+// previous half-step scattered its products into this side's entry order
+// (t_scatter), else through the entry map
 __device__ __forceinline__ int64_t t_index(const klnmf_solve_args_t &a, int64_t q) {
-    const int64_t i = a.tmap ? (int64_t)a.tmap[q] : q;
+    const int64_t i = (a.tmap && !a.t_scatter) ? (int64_t)a.tmap[q] : q;
     kcheck(i >= 0 && i < a.side.nnz, 3);
     return i;
 }
@@ -331,11 +333,17 @@ __device__ __forceinline__ void put_moving(const klnmf_solve_args_t &a, float *m
     moving[i] = v;
     for (int p = 0; p < a.n_peers; ++p) static_cast<float *>(a.peer_moving[p])[i] = v;
 }
+// (t_scatter: the product of entry i lands at its position in the other
+// side's entry order, where the next half-step reads it coalesced; the
+// stores are fire-and-forget, the subproblem start no longer waits on a
+// dependent gather through the map)
 __device__ __forceinline__ void put_t(const klnmf_solve_args_t &a, int64_t i, double v) {
     kcheck(i >= 0 && i < a.side.nnz, 5);
     kcheck(v >= 0.0 && v < INFINITY, 9);
-    a.t_out[i] = v;
-    for (int p = 0; p < a.n_peers; ++p) a.peer_t[p][i] = v;
+    const int64_t o = (a.tmap && a.t_scatter) ? (int64_t)a.tmap[i] : i;
+    kcheck(o >= 0 && o < a.side.nnz, 5);
+    a.t_out[o] = v;
+    for (int p = 0; p < a.n_peers; ++p) a.peer_t[p][o] = v;
 }
 
 // After a thread's last peer store of the half-step: order its NVLink stores
@@ -710,7 +718,9 @@ __global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(co
     const int s = (int)(a.side.ptr[j + 1] - lo);
 
     for (int k = tid; k < r; k += NT) ssum[k] = a.sum_pos[k];
-    for (int k = tid; k < r; k += NT) xs[k] = moving[j * rp + a.perm_in[k]];
+    // the result row starts as the input row (batched entry tests: only
+    // coordinates that enter the Newton loop write it)
+    for (int k = tid; k < r; k += NT) xs[k] = xo[k] = moving[j * rp + a.perm_in[k]];
 
     double u[NPL], vi[NPL];
     int roff[NPL];
@@ -762,6 +772,7 @@ __global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(co
         const uint32_t perm = counter ? chunk_perm4(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, ch)
                                       : PERM4_IDENTITY;
         bool fresh = false;
+        unsigned emask = 0;  // slots of this chunk whose coordinate enters (valid while fresh)
 #pragma unroll 1
         for (int cc = 0; cc < nc; ++cc) {
             const int q = (int)((perm >> (2 * cc)) & 3u);  // chunk coordinate visited in slot cc
@@ -783,7 +794,23 @@ __global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(co
                 cur = buf;
                 buf ^= 1;
                 fresh = true;
+                // entry tests of the slots cc..nc-1 at once (lane l of every warp
+                // tests slot cc + l, same expressions as the visit below); the
+                // mask is identical in every warp, so the skip is block-uniform
+                const int sl = cc + (tid & 31);
+                bool ent = false;
+                if (sl < nc) {
+                    const int qs = (int)((perm >> (2 * sl)) & 3u);
+                    const int ts = pc * C + qs;
+                    if (!counter || ts < r) {
+                        const double xv = (double)xs[ts];
+                        const double bv = ssum[ts] + pm.beta;
+                        ent = enters((bv + pm.alpha * xv) - bs.get(cur, qs), xv, pm.eps_grad);
+                    }
+                }
+                emask = (__ballot_sync(FULL_MASK, ent) & 0xFu) << cc;
             }
+            if (!((emask >> cc) & 1u)) continue;  // x unchanged, xo = xs already
             double x = (double)xs[tt];
             const double base = ssum[tt] + pm.beta;
             double g = (base + pm.alpha * x) - bs.get(cur, q);

@@ -366,6 +366,36 @@ class DevicePlan:
                     if any(sp.coop is not None and sp.coop[5] for sp in self.sides.values()):
                         self.scratch = torch.empty(4 * max(self.nnz, 1), dtype=torch.float64, device=dev)
 
+        # maintained-product layout (klnmf_solve_args_t.t_scatter): each
+        # half-step scatters its products into the other side's entry order,
+        # so the next half-step reads them coalesced; the all-gather exchange
+        # moves contiguous entry ranges and keeps the gathered layout
+        self.t_scatter = bool(self.fp32 and (self.world == 1 or self._peers is not None)
+                              and os.environ.get("KLNMF_T_SCATTER", "1") != "0")
+
+    def t_orient(self, which: str) -> tuple[str, str]:
+        """(read, write) maintained-product arrays of a half-step ("csc" /
+        "csr": the entry order each array is stored in)."""
+        if self.t_scatter:
+            return ("csc", "csr") if which == "F" else ("csr", "csc")
+        return ("csr", "csc") if which == "F" else ("csc", "csr")
+
+    def t_entries(self, which: str, name: str) -> torch.Tensor:
+        """Maintained products of array `name` in side `which`'s entry order
+        (a fresh device tensor)."""
+        own = "csc" if which == "F" else "csr"
+        t = self.t[name][: self.nnz]
+        return t.clone() if name == own else t[self.sides[which].tmap.long()]
+
+    def set_t_entries(self, which: str, name: str, values) -> None:
+        """Store products given in side `which`'s entry order into array `name`."""
+        own = "csc" if which == "F" else "csr"
+        v = torch.as_tensor(values, dtype=torch.float64).to(self.dev)
+        if name == own:
+            self.t[name][: self.nnz].copy_(v)
+        else:
+            self.t[name][self.sides[which].tmap.long()] = v
+
     # ------------------------------------------------------------------
     @staticmethod
     def _new_event():
@@ -704,7 +734,7 @@ class DevicePlan:
             sp[: self.r] = np.asarray(sums_pos, dtype=np.float64)
             self.sum_pos.copy_(torch.from_numpy(sp))
         if self.fp32:
-            need = "csr" if which == "F" else "csc"
+            need = self.t_orient(which)[0]
             if self.t_current != need:
                 self._init_t(need)
         if self._peers is not None:
@@ -724,7 +754,7 @@ class DevicePlan:
         else:
             self._launch(which, alpha, beta, tol, dev_sums, events)
         if self.fp32:
-            self.t_current = "csc" if which == "F" else "csr"
+            self.t_current = self.t_orient(which)[1]
         self.order[which] = np.asarray(out_order, dtype=np.int64).copy()
         if self.world > 1:
             torch.cuda.nvtx.range_push(f"klnmf.exchange.{which}")
@@ -811,14 +841,15 @@ class DevicePlan:
         a.order_seed = self.order_seed
         a.order_iter = self._perm[3].data_ptr()
         if self.fp32:
-            need = "csr" if which == "F" else "csc"
+            t_in, t_out = self.t_orient(which)
             a.tmap = side.tmap.data_ptr()
-            a.t_in = self.t[need].data_ptr()
-            a.t_out = self.t["csc" if which == "F" else "csr"].data_ptr()
+            a.t_in = self.t[t_in].data_ptr()
+            a.t_out = self.t[t_out].data_ptr()
+            a.t_scatter = int(self.t_scatter)
             if self._peers is not None:
                 a.n_peers = self.world - 1
                 a.peer_moving = self._peers[which].data_ptr()
-                a.peer_t = self._peers["csc" if which == "F" else "csr"].data_ptr()
+                a.peer_t = self._peers[t_out].data_ptr()
         item_base = side.items.data_ptr()
         lib = _lib.load()
         main = self.stream_ptr
@@ -888,7 +919,8 @@ class DevicePlan:
         allgather_ranges(self.factors[which], side.ranges, self.group)
         if self.fp32:
             eranges = [(int(side.ptr_host[lo]), int(side.ptr_host[hi])) for lo, hi in side.ranges]
-            allgather_ranges(self.t["csc" if which == "F" else "csr"], eranges, self.group)
+            assert not self.t_scatter  # ranges are contiguous in this side's entry order
+            allgather_ranges(self.t[self.t_orient(which)[1]], eranges, self.group)
 
     # ------------------------------------------------------------------
     def take_stats(self) -> SolveStats:
@@ -920,9 +952,11 @@ class DevicePlan:
         data = ctypes.c_double()
         if self.fp32 and self.t_current is not None and not from_factors:
             # fp32 mode carries t = <W_i, F_j> for every entry (all ranks hold all
-            # of it after the exchange): one streaming pass over (v, t)
-            side = self.sides["F"] if self.t_current == "csc" else self.sides["W"]
-            _lib.call("klnmf_kl_data_term_t", side.val.data_ptr(), self.t[self.t_current].data_ptr(),
+            # of it after the exchange): one streaming pass over (v, t), summed
+            # in V's CSC entry order whichever orientation t is carried in
+            side = self.sides["F"]
+            tmap = 0 if self.t_current == "csc" else side.tmap.data_ptr()
+            _lib.call("klnmf_kl_data_term_t_mapped", side.val.data_ptr(), self.t[self.t_current].data_ptr(), tmap,
                       self.nnz, float(eps_div), ctypes.byref(data), self.stream_ptr)
         else:
             side = self.sides["F"]

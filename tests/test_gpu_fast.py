@@ -125,12 +125,10 @@ def _device_state(plan, which):
     val = side.val.cpu().numpy()
     fixed = plan.factors[fixed_name].cpu().numpy()
     moving = plan.factors[which].cpu().numpy()
-    need = "csr" if which == "F" else "csc"
+    need = plan.t_orient(which)[0]
     if plan.t_current != need:
         plan._init_t(need)
-    t_in = plan.t[need].cpu().numpy()
-    tmap = side.tmap.cpu().numpy()
-    return ptr, idx, val, fixed, moving, t_in[tmap]
+    return ptr, idx, val, fixed, moving, plan.t_entries(which, need).cpu().numpy()
 
 
 def _compare_half_step(plan, which, ids, alpha, beta, iteration=None):
@@ -151,7 +149,7 @@ def _compare_half_step(plan, which, ids, alpha, beta, iteration=None):
     plan.half_step(which, ids, alpha=alpha, beta=beta, iteration=iteration)
     st_gpu = plan.take_stats()
     mov_gpu = plan.factors[which].cpu().numpy()
-    t_gpu = plan.t["csc" if which == "F" else "csr"].cpu().numpy()[: plan.nnz]
+    t_gpu = plan.t_entries(which, plan.t_orient(which)[1]).cpu().numpy()
     return mov_gpu, mov_or, t_gpu, t_or, st_gpu, st_or
 
 
@@ -366,10 +364,10 @@ def test_fp32_iterations_per_half_step(cuda_ok, name, m):
         for which, a, b in (("F", reg.alpha2, reg.beta2), ("W", reg.alpha1, reg.beta1)):
             side = plan.sides[which]
             fixed_name = "W" if which == "F" else "F"
-            need = "csr" if which == "F" else "csc"
+            need, out = plan.t_orient(which)
             if plan.t_current != need:
                 plan._init_t(need)
-            t0 = plan.t[need].cpu().numpy()[side.tmap.cpu().numpy()]
+            t0 = plan.t_entries(which, need).cpu().numpy()
             fixed = plan.factors[fixed_name].cpu().numpy()
             mov = plan.factors[which].cpu().numpy()
             mov_vis = np.zeros_like(mov)
@@ -383,13 +381,13 @@ def test_fp32_iterations_per_half_step(cuda_ok, name, m):
             sg = plan.take_stats()
             got = plan.factors[which].cpu().numpy()
             got_vis = got[:, np.argsort(out_order)[ids]]
-            tg = plan.t["csc" if which == "F" else "csr"].cpu().numpy()[: plan.nnz]
+            tg = plan.t_entries(which, out).cpu().numpy()
             _check(got_vis, mo[:, :r], tg, to, f"{name} it{it + 1} {which}")
             _check_stats(sg, so)
             reset = np.zeros_like(got)
             reset[:, np.argsort(out_order)[ids]] = mo[:, :r]
             plan.factors[which].copy_(torch.from_numpy(reset))
-            plan.t["csc" if which == "F" else "csr"][: plan.nnz].copy_(torch.from_numpy(to))
+            plan.set_t_entries(which, out, torch.from_numpy(to))
         ids = nxt
 
 
