@@ -158,8 +158,9 @@ typedef struct {
     const int32_t *tmap;      /* nnz: position of each entry in the other side's entry order */
     const double *t_in;       /* nnz (see t_scatter) */
     double *t_out;            /* nnz (see t_scatter) */
-    double *scratch;          /* exact mode: nnz doubles; fp32 long-row kernels: 4*nnz (a 32-byte
-                                 record per entry, used only by entries beyond the on-chip capacity) */
+    double *scratch;          /* exact mode: nnz doubles; fp32 long-row kernels: 4*nnz + ceil(nnz/8)
+                                 (a 32-byte record and a one-byte chunk mask per entry, used only by
+                                 entries beyond the on-chip capacity) */
     int32_t r;
     int32_t rp;
     double alpha, beta, eps_grad, eps_x, eps_div;
@@ -247,6 +248,9 @@ int klnmf_row_sums_fast(const float *fac, int64_t n_items, int32_t rp, int32_t r
  * order[tt] = natural coordinate stored at position tt (tt < r). */
 int klnmf_layout_to_device(const double *src, int64_t r, int64_t n, const int32_t *order,
                            int32_t rp, void *dst, int fp32, void *stream);
+/* the same from an fp32 (r, n) source (fp32 storage only) */
+int klnmf_layout_to_device_f32src(const float *src, int64_t r, int64_t n, const int32_t *order, int32_t rp,
+                                  float *dst, void *stream);
 int klnmf_layout_from_device(const void *src, int64_t r, int64_t n, const int32_t *order,
                              int32_t rp, int fp32, double *dst, void *stream);
 /* fp32 factor (item-major, visit order) -> (r, n) natural-order fp32: the

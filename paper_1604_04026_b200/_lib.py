@@ -55,6 +55,7 @@ EXPORTS = (
     "klnmf_row_sums_exact",
     "klnmf_row_sums_fast",
     "klnmf_layout_to_device",
+    "klnmf_layout_to_device_f32src",
     "klnmf_layout_from_device",
     "klnmf_layout_from_device_f32",
     "klnmf_transpose",
@@ -166,6 +167,7 @@ _SIGS = {
     "klnmf_row_sums_exact": ([P, I64, I32, I32, P, P], INT),
     "klnmf_row_sums_fast": ([P, I64, I32, I32, P, P], INT),
     "klnmf_layout_to_device": ([P, I64, I64, P, I32, P, INT, P], INT),
+    "klnmf_layout_to_device_f32src": ([P, I64, I64, P, I32, P, P], INT),
     "klnmf_layout_from_device": ([P, I64, I64, P, I32, INT, P, P], INT),
     "klnmf_layout_from_device_f32": ([P, I64, I64, P, I32, P, P], INT),
     "klnmf_transpose": ([P, P, P, INT, I64, I64, I64, P, P, P, P, P, P], INT),

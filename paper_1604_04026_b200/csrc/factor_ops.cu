@@ -10,8 +10,8 @@
 namespace klnmf {
 namespace {
 
-template <typename T>
-__global__ void to_device_kernel(const double *src, int64_t r, int64_t n, const int32_t *order,
+template <typename T, typename S = double>
+__global__ void to_device_kernel(const S *src, int64_t r, int64_t n, const int32_t *order,
                                  int32_t rp, T *dst) {
     // dst[i, tt] = src[order[tt], i]; padding columns = 0
     const int64_t total = n * rp;
@@ -147,6 +147,17 @@ extern "C" int klnmf_layout_to_device(const double *src, int64_t r, int64_t n, c
     else
         to_device_kernel<double><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, r, n, order, rp,
                                                                                      static_cast<double *>(dst));
+    KLNMF_CHECK_LAUNCH("to_device_kernel");
+    return 0;
+}
+
+// the same from fp32 values already narrowed on the host (fp32 mode: half the
+// PCIe bytes; host (float)x and device __double2float_rn round alike)
+extern "C" int klnmf_layout_to_device_f32src(const float *src, int64_t r, int64_t n, const int32_t *order,
+                                             int32_t rp, float *dst, void *stream) {
+    const int64_t total = n * rp;
+    if (total == 0) return 0;
+    to_device_kernel<float, float><<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(src, r, n, order, rp, dst);
     KLNMF_CHECK_LAUNCH("to_device_kernel");
     return 0;
 }

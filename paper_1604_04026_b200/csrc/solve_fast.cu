@@ -889,12 +889,74 @@ constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
 constexpr int CL_MAXG = CL_PER_SM > 2 ? 1024 : 512;  // most CTAs in one cooperative row group
 constexpr size_t COOP_GROUP_BYTES = 2 * CL_MAXG * NV * 2 * sizeof(unsigned long long) + 128;
 
-// Per-entry record of the spilled entries of the long-row kernels (scratch).
+// Record of a spilled entry of the long-row kernels (scratch): u, 1/v and
+// the current chunk's four fixed-factor values -- one 32-byte sector, so a
+// warp's consecutive entries stream whole sectors (a structure-of-arrays
+// layout, reading only the components a pass or move uses, measured 3.7%
+// slower on C5's spilled rows: more requests for the same sectors).  Next
+// to the records (after 4*nnz doubles), one byte per entry holds the chunk's
+// nonzero mask (bit c: a_c != 0), written by the stage: a pass over
+// coordinates c0..3 reads only the records with a nonzero among them, a move
+// or re-evaluation of coordinate q only those with a_q != 0 (78-85% of the
+// fixed factors are zeros; a zero term adds exactly 0 and leaves u exactly
+// unchanged), and a move writes back only what it changed.  The loops are
+// kept out of line: they run only for rows longer than the on-chip capacity
+// of their CTAs, and inlined they raised the register pressure (spills) of
+// every long-row slice (out of line: C4 -1.0%).
 struct __align__(32) SpillRec {
     double2 uv;  // u = v/(t+eps), vi = 1/v
     float4 a;    // the current chunk of the entry's fixed-factor row
 };
 static_assert(sizeof(SpillRec) == 32, "one 32-byte sector per spilled entry");
+struct P8 {
+    double v[NV];
+};
+struct P2 {
+    double g, h;
+};
+// the chunk's fixed-factor slice of every spilled entry i0, i0 + step, ... < cn
+__device__ __noinline__ void spill_stage(SpillRec *rec, uint8_t *mask, int64_t i0, int64_t cn, int64_t step,
+                                        const float *fixed, const int32_t *idx, int64_t n_fix, int rp, int pc) {
+#pragma unroll 4
+    for (int64_t i = i0; i < cn; i += step) {
+        const int32_t row = idx[i];
+        kcheck(row >= 0 && row < n_fix, 1);
+        const float4 a4 = ldg_f4(fixed + (int64_t)row * rp + pc * C);
+        const unsigned m = (a4.x != 0.f ? 1u : 0u) | (a4.y != 0.f ? 2u : 0u) | (a4.z != 0.f ? 4u : 0u) |
+                           (a4.w != 0.f ? 8u : 0u);
+        mask[i] = (uint8_t)m;
+        if (m) __stcg(&rec[i].a, a4);
+    }
+}
+// partials of the chunk's coordinates c0..3 over the spilled entries, added to acc
+__device__ __noinline__ P8 spill_pass(const SpillRec *rec, const uint8_t *mask, int64_t i0, int64_t cn,
+                                     int64_t step, int c0, P8 acc) {
+#pragma unroll 4
+    for (int64_t i = i0; i < cn; i += step) {
+        if ((__ldcg(mask + i) >> c0) == 0) continue;  // a_c0..a_3 all zero: adds exactly 0
+        const double2 uv = __ldcg(&rec[i].uv);
+        accum_chunk(acc.v, __ldcg(&rec[i].a), uv.x, entry_z(uv.x, uv.y), c0);
+    }
+    return acc;
+}
+// a move of coordinate q by delta (upd) and/or its re-evaluation partials
+// (again, added to acc) over the spilled entries
+__device__ __noinline__ P2 spill_move(SpillRec *rec, const uint8_t *mask, int64_t i0, int64_t cn, int64_t step,
+                                     int q, double delta, bool upd, bool again, bool clamp, double eps, P2 acc) {
+#pragma unroll 4
+    for (int64_t i = i0; i < cn; i += step) {
+        if (!((__ldcg(mask + i) >> q) & 1u)) continue;  // a_q == 0: u unchanged, contributes exactly 0
+        const double av = (double)__ldcg(reinterpret_cast<const float *>(&rec[i].a) + q);
+        double2 uv = __ldcg(&rec[i].uv);
+        if (upd) {
+            if (clamp) entry_update<true>(delta, av, eps, uv.x, uv.y);
+            else entry_update<false>(delta, av, eps, uv.x, uv.y);
+            __stcg(&rec[i].uv, uv);
+        }
+        if (again) accum(acc.g, acc.h, uv.x, entry_z(uv.x, uv.y), av);
+    }
+    return acc;
+}
 
 struct GroupRed {
     double wred[2][CL_NT / 32][NV];
@@ -1150,10 +1212,11 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                                                              : (int)min((cn + NT - 1) / NT, (int64_t)(NR + NS));
     const double eps = pm.eps_div;
     // spilled entries (rows longer than the on-chip capacity of their CTAs):
-    // one 32-byte record per entry in scratch -- (u, vi) and the current
+    // a 32-byte record per entry in scratch -- (u, vi) and the current
     // chunk's 4 fixed-factor values, staged once per chunk -- so every pass
     // and move streams whole sectors instead of re-gathering the fixed factor
     SpillRec *UVg = reinterpret_cast<SpillRec *>(a.scratch) + base;
+    uint8_t *UVm = reinterpret_cast<uint8_t *>(a.scratch + 4 * a.side.nnz) + base;  // chunk nonzero masks
 
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
@@ -1188,10 +1251,10 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     const int64_t spill0 = (int64_t)(NR + NS) * NT;  // first spilled local entry
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const int64_t g = base + i;
-        double2 uv;
-        entry_init(a.t_in[t_index(a, g)], val[g], eps, uv.x, uv.y);
+        double uu, vv;
+        entry_init(a.t_in[t_index(a, g)], val[g], eps, uu, vv);
         kcheck(base + i < a.side.nnz, 8);
-        UVg[i].uv = uv;
+        UVg[i].uv = make_double2(uu, vv);
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
     const int nchunks = (r + C - 1) / C;
@@ -1217,8 +1280,8 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         // spilled entries: stage the chunk's slice next to their state
         // (each thread stages and later reads only its own records)
 #pragma unroll 4
-        for (int64_t i = spill0 + tid; i < cn; i += NT)
-            __stcg(&UVg[i].a, ldg_f4(fixed + (int64_t)gather_off(a, base + i) + pc * C));
+        if (cn > spill0)
+            spill_stage(UVg, UVm, spill0 + tid, cn, NT, fixed, a.side.idx + base, a.side.n_fix, rp, pc);
         cp_wait<0>();
         ph.mark(1);
         const float4 *A = cache + tid;
@@ -1247,10 +1310,13 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                         accum_from<CC>(red, A[(NR + e) * NT], uu, entry_z(uu, VIs[e * NT + tid]));
                     }
                 });
-#pragma unroll 4
-                for (int64_t i = spill0 + tid; i < cn; i += NT) {
-                    const double2 uv = __ldcg(&UVg[i].uv);
-                    accum_chunk(red, __ldcg(&UVg[i].a), uv.x, entry_z(uv.x, uv.y), counter ? 0 : cc);
+                if (cn > spill0) {  // CTA-uniform
+                    P8 acc;
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) acc.v[i] = red[i];
+                    acc = spill_pass(UVg, UVm, spill0 + tid, cn, NT, counter ? 0 : cc, acc);
+#pragma unroll
+                    for (int i = 0; i < NV; ++i) red[i] = acc.v[i];
                 }
                 ph.mark(2);
                 reduce(red, buf);
@@ -1298,17 +1364,11 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
                             }
                             if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
                         }
-#pragma unroll 4
-                        for (int64_t i = spill0 + tid; i < cn; i += NT) {
-                            const double av = (double)__ldcg(reinterpret_cast<const float *>(&UVg[i].a) + q);
-                            double2 uv = __ldcg(&UVg[i].uv);
-                            double &uu = uv.x;
-                            const double vv = uv.y;
-                            if (upd) {
-                                entry_update<CL>(delta, av, eps, uu, vv);
-                                __stcg(&UVg[i].uv, uv);
-                            }
-                            if (again) accum(g2, h2, uu, entry_z(uu, vv), av);
+                        if (cn > spill0) {  // CTA-uniform
+                            const P2 acc = spill_move(UVg, UVm, spill0 + tid, cn, NT, q, delta, upd, again, CL, eps,
+                                                      P2{g2, h2});
+                            g2 = acc.g;
+                            h2 = acc.h;
                         }
                     });
                     ph.mark(5);

@@ -99,6 +99,12 @@ SPILL_NS = 1.2
 ON_CHIP_ENTRIES = 296 * 4096  # cooperative kernel: CTAs x entries per CTA
 
 
+def spill_scratch_doubles(nnz: int) -> int:
+    """Scratch of the long-row kernels' spilled entries: a 32-byte record and
+    a one-byte chunk mask per entry of the side (klnmf_solve_args_t.scratch)."""
+    return 4 * nnz + (nnz + 7) // 8
+
+
 def subproblem_cost(sizes: np.ndarray) -> np.ndarray:
     """Modelled device time (ns) of each subproblem of a half-step."""
     sizes = np.asarray(sizes, dtype=np.int64)
@@ -321,7 +327,8 @@ class DevicePlan:
                 # longer than the whole GPU's on-chip capacity, long-row
                 # bucket): a 32-byte record per entry
                 need_spill = any(s.coop is not None and s.coop[5] for s in self.sides.values())
-                self.scratch = torch.empty(4 * nz if need_spill else 4, dtype=torch.float64, device=dev)
+                self.scratch = torch.empty(spill_scratch_doubles(nz) if need_spill else 4, dtype=torch.float64,
+                                           device=dev)
             else:
                 self.t = None
                 self.scratch = torch.empty(nz, dtype=torch.float64, device=dev)
@@ -364,7 +371,8 @@ class DevicePlan:
                                                            sp.ptr_host, sp.tmap)
                         self._build_coop(self.sides[name])
                     if any(sp.coop is not None and sp.coop[5] for sp in self.sides.values()):
-                        self.scratch = torch.empty(4 * max(self.nnz, 1), dtype=torch.float64, device=dev)
+                        self.scratch = torch.empty(spill_scratch_doubles(max(self.nnz, 1)), dtype=torch.float64,
+                                                   device=dev)
 
         # maintained-product layout (klnmf_solve_args_t.t_scatter): each
         # half-step scatters its products into the other side's entry order,
@@ -603,11 +611,17 @@ class DevicePlan:
             arr = np.ascontiguousarray(arr, dtype=np.float64)
             if arr.shape != (self.r, n_items):
                 raise ValueError(f"{name} must have shape {(self.r, n_items)}")
-            src = torch.empty(self.r, n_items, dtype=torch.float64, device=self.dev)
-            _lib.call("klnmf_upload_f64", arr.ctypes.data, arr.size, src.data_ptr(), self.stream_ptr)
             o = torch.from_numpy(self._padded(order)).to(self.dev)
-            _lib.call("klnmf_layout_to_device", src.data_ptr(), self.r, n_items, o.data_ptr(), self.rp,
-                      self.factors[name].data_ptr(), int(self.fp32), self.stream_ptr)
+            if self.fp32:  # narrowed on host threads: half the bytes over PCIe
+                src = torch.empty(self.r, n_items, dtype=torch.float32, device=self.dev)
+                _lib.call("klnmf_upload_f64_as_f32", arr.ctypes.data, arr.size, src.data_ptr(), self.stream_ptr)
+                _lib.call("klnmf_layout_to_device_f32src", src.data_ptr(), self.r, n_items, o.data_ptr(), self.rp,
+                          self.factors[name].data_ptr(), self.stream_ptr)
+            else:
+                src = torch.empty(self.r, n_items, dtype=torch.float64, device=self.dev)
+                _lib.call("klnmf_upload_f64", arr.ctypes.data, arr.size, src.data_ptr(), self.stream_ptr)
+                _lib.call("klnmf_layout_to_device", src.data_ptr(), self.r, n_items, o.data_ptr(), self.rp,
+                          self.factors[name].data_ptr(), 0, self.stream_ptr)
             self.order[name] = np.asarray(order, dtype=np.int64).copy()
         self.t_current = None
 
