@@ -884,6 +884,9 @@ namespace cg = cooperative_groups;
 #define KLNMF_CL_NT 256
 #define KLNMF_CL_PER_SM 2
 #endif
+#ifndef KLNMF_CL_OFF_SMEM  // long-row kernels: the shared-memory entries' gather offsets in shared memory (C4 -1.4%)
+#define KLNMF_CL_OFF_SMEM 1
+#endif
 constexpr int CL_NT = KLNMF_CL_NT, CL_NR = 8, CL_NS = 8, CL_PER_SM = KLNMF_CL_PER_SM;
 constexpr int CL_NE = CL_NR + CL_NS;  // resident entries per thread
 constexpr int CL_MAXG = CL_PER_SM > 2 ? 1024 : 512;  // most CTAs in one cooperative row group
@@ -1186,7 +1189,10 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
     float4 *cache = reinterpret_cast<float4 *>(smem_raw);             // [NR+NS][NT]: current chunk
     double *Us = reinterpret_cast<double *>(cache + (NR + NS) * NT);  // [NS][NT]
     double *VIs = Us + NS * NT;                                       // [NS][NT]
-    float *xs = reinterpret_cast<float *>(VIs + NS * NT);             // [2][rps]: input row, result
+    // gather offsets of the shared-memory entries: in shared memory too
+    // (KLNMF_CL_OFF_SMEM), or in registers
+    int *Offs = reinterpret_cast<int *>(VIs + NS * NT);                          // [NS][NT] if in smem
+    float *xs = reinterpret_cast<float *>(Offs + (KLNMF_CL_OFF_SMEM ? NS * NT : 0));  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
     uint8_t *cord = reinterpret_cast<uint8_t *>(xo + (a.rp | 1));  // counter order
 
@@ -1234,17 +1240,21 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             u[e] = vi[e] = 0.0;
         }
     }
-    int offs[NS];
+    int offs_r[KLNMF_CL_OFF_SMEM ? 1 : NS];
+    auto offs = [&](int e) -> int & {
+        if constexpr (KLNMF_CL_OFF_SMEM) return Offs[e * NT + tid];
+        else return offs_r[e];
+    };
 #pragma unroll
     for (int e = 0; e < NS; ++e) {
         const int64_t i = tid + (int64_t)(NR + e) * NT;
         const int si = e * NT + tid;
         if (i < cn) {
             const int64_t g = base + i;
-            offs[e] = gather_off(a, g);
+            offs(e) = gather_off(a, g);
             entry_init(a.t_in[t_index(a, g)], val[g], eps, Us[si], VIs[si]);
         } else {
-            offs[e] = -1;
+            offs(e) = -1;
             Us[si] = VIs[si] = 0.0;
         }
     }
@@ -1275,7 +1285,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
 #pragma unroll
         for (int e = 0; e < NS; ++e)
             if (NR + e < ne)
-                cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs[e], 0) + pc * C, offs[e] >= 0);
+                cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs(e), 0) + pc * C, offs(e) >= 0);
         cp_commit();
         // spilled entries: stage the chunk's slice next to their state
         // (each thread stages and later reads only its own records)
@@ -1399,7 +1409,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         if (off[e] >= 0) put_t(a, base + tid + (int64_t)e * NT, entry_t(u[e], vi[e], eps));
 #pragma unroll
     for (int e = 0; e < NS; ++e)
-        if (offs[e] >= 0)
+        if (offs(e) >= 0)
             put_t(a, base + tid + (int64_t)(NR + e) * NT, entry_t(Us[e * NT + tid], VIs[e * NT + tid], eps));
     for (int64_t i = spill0 + tid; i < cn; i += NT) {
         const double2 uv = UVg[i].uv;
@@ -1498,7 +1508,8 @@ constexpr int kNumFast = sizeof(kFast) / sizeof(kFast[0]);
 
 inline size_t slice_smem(int rp) {
     return (size_t)CL_NE * CL_NT * sizeof(float4) + (size_t)CL_NS * CL_NT * 2 * sizeof(double) +
-           2 * sizeof(float) * (size_t)(rp | 1) + MAX_CHUNKS + 16;
+           (KLNMF_CL_OFF_SMEM ? (size_t)CL_NS * CL_NT * sizeof(int) : 0) + 2 * sizeof(float) * (size_t)(rp | 1) +
+           MAX_CHUNKS + 16;
 }
 
 }  // namespace
