@@ -441,14 +441,24 @@ struct PhaseClock {
 constexpr int warp_minb(int npl) {
     return npl <= 7 ? KLNMF_WARP_MINB_SMALL : (npl <= KLNMF_WARP_MINB_NPL ? KLNMF_WARP_MINB : KLNMF_WARP_MINB_LARGE);
 }
+// Gather offsets of the entries in shared memory instead of registers
+// (KLNMF_ROFF_SMEM) for the warp kernels whose blocks per SM it does not cut
+// at rp <= 128 (the NPL = 8, 12, 16 rings leave no room): registers freed
+// under the cap, C4 -1.0% (A/B, two repetitions).
+#ifndef KLNMF_ROFF_SMEM
+#define KLNMF_ROFF_SMEM 1
+#endif
+constexpr bool warp_roff_smem(int npl) { return KLNMF_ROFF_SMEM && (npl <= 7 || npl == 10 || npl == 14); }
 template <int L, int NPL, bool CTR>
 __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const klnmf_solve_args_t a) {
     constexpr int NT = 128;
     constexpr int GPB = NT / L;  // groups per block
     constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool RS = warp_roff_smem(NPL);
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);                 // [STAGES][NPL][NT]
-    float *xs_all = reinterpret_cast<float *>(ring + STAGES * NPL * NT);  // [GPB][2][rps]
+    int *sroff = reinterpret_cast<int *>(ring + STAGES * NPL * NT);        // [NPL][NT] if RS
+    float *xs_all = reinterpret_cast<float *>(sroff + (RS ? NPL * NT : 0));  // [GPB][2][rps]
     // counter order only: [GPB][MAX_CHUNKS] visit order of each group's chunks
     uint8_t *cord_all = reinterpret_cast<uint8_t *>(xs_all + GPB * 2 * (a.rp | 1));
     __shared__ double ssum[KMAX_RP];  // fixed-factor row sums by position
@@ -493,16 +503,20 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
     __syncwarp();
 
     double u[NPL], vi[NPL];
-    int roff[NPL];  // gather source of each entry (row 0 for absent entries)
+    int roff_r[RS ? 1 : NPL];  // gather source of each entry (row 0 for absent entries)
+    auto roff = [&](int e) -> int & {
+        if constexpr (RS) return sroff[e * NT + tid];
+        else return roff_r[e];
+    };
 #pragma unroll
     for (int e = 0; e < NPL; ++e) {
         const int p = gl + e * L;
         if (p < s) {
             const int64_t q = lo + p;
-            roff[e] = gather_off(a, q);
+            roff(e) = gather_off(a, q);
             entry_init(a.t_in[t_index(a, q)], val[q], pm.eps_div, u[e], vi[e]);
         } else {
-            roff[e] = 0;
+            roff(e) = 0;
             u[e] = vi[e] = 0.0;  // contributes exactly 0 to every sum
         }
     }
@@ -514,7 +528,7 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
             const int pc = phys(chunk);
 #pragma unroll
             for (int e = 0; e < NPL; ++e)
-                cp_async16(base + 16u * NT * e, fixed + roff[e] + pc * C, gl + e * L < s);
+                cp_async16(base + 16u * NT * e, fixed + roff(e) + pc * C, gl + e * L < s);
         }
         cp_commit();
     };
@@ -693,12 +707,20 @@ constexpr int block_minb(int nt, int npl) {
     const int cap = npl <= KLNMF_BLOCK_SMALL_NPL ? KLNMF_BLOCK_MAXREG_SMALL : KLNMF_BLOCK_MAXREG;
     return cap > 0 ? (65536 / (nt * cap) > 0 ? 65536 / (nt * cap) : 1) : 1;
 }
+#ifndef KLNMF_BROFF_SMEM  // the same for the block kernels that keep their blocks per SM (C4 -0.9%)
+#define KLNMF_BROFF_SMEM 1
+#endif
+constexpr bool block_roff_smem(int nt, int npl) {
+    return KLNMF_BROFF_SMEM && (npl == 10 || npl == 14 || (nt == 256 && npl == 16));
+}
 template <int NT, int NPL, bool CTR>
 __global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(const klnmf_solve_args_t a) {
     constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *ring = reinterpret_cast<float4 *>(smem_raw);             // [STAGES][NPL][NT]
-    float *xs = reinterpret_cast<float *>(ring + STAGES * NPL * NT);  // [2][rps]: input row, result
+    constexpr bool RS = block_roff_smem(NT, NPL);
+    int *sroff = reinterpret_cast<int *>(ring + STAGES * NPL * NT);      // [NPL][NT] if RS
+    float *xs = reinterpret_cast<float *>(sroff + (RS ? NPL * NT : 0));  // [2][rps]: input row, result
     float *xo = xs + (a.rp | 1);
     uint8_t *cord = reinterpret_cast<uint8_t *>(xo + (a.rp | 1));  // counter order only
     __shared__ double ssum[KMAX_RP];
@@ -723,16 +745,20 @@ __global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(co
     for (int k = tid; k < r; k += NT) xs[k] = xo[k] = moving[j * rp + a.perm_in[k]];
 
     double u[NPL], vi[NPL];
-    int roff[NPL];
+    int roff_r[RS ? 1 : NPL];
+    auto roff = [&](int e) -> int & {
+        if constexpr (RS) return sroff[e * NT + tid];
+        else return roff_r[e];
+    };
 #pragma unroll
     for (int e = 0; e < NPL; ++e) {
         const int p = tid + e * NT;
         if (p < s) {
             const int64_t q = lo + p;
-            roff[e] = gather_off(a, q);
+            roff(e) = gather_off(a, q);
             entry_init(a.t_in[t_index(a, q)], val[q], pm.eps_div, u[e], vi[e]);
         } else {
-            roff[e] = 0;
+            roff(e) = 0;
             u[e] = vi[e] = 0.0;
         }
     }
@@ -750,7 +776,7 @@ __global__ void __launch_bounds__(NT, block_minb(NT, NPL)) solve_block_kernel(co
             const int pc = phys(chunk);
 #pragma unroll
             for (int e = 0; e < NPL; ++e)
-                cp_async16(base + 16u * NT * e, fixed + roff[e] + pc * C, tid + e * NT < s);
+                cp_async16(base + 16u * NT * e, fixed + roff(e) + pc * C, tid + e * NT < s);
         }
         cp_commit();
     };
@@ -1477,14 +1503,17 @@ struct FastKernel {
     int gpb;           // subproblems per block
     int ring_entries;  // float4 ring slots per thread and stage (NPL)
     int cluster;       // CTAs per subproblem (cluster kernel), 0 = plain launch, -1 = cooperative
+    bool roff_smem;    // gather offsets in shared memory (warp_roff_smem)
 };
 
 #define WK(L, NPL) \
-    {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL, false>, solve_warp_kernel<L, NPL, true>, 128 / (L), NPL, 0}
+    {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL, false>, solve_warp_kernel<L, NPL, true>, 128 / (L), NPL, 0, \
+     warp_roff_smem(NPL)}
 #define BK(NT, NPL) \
-    {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL, false>, solve_block_kernel<NT, NPL, true>, 1, NPL, 0}
+    {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL, false>, solve_block_kernel<NT, NPL, true>, 1, NPL, 0, \
+     block_roff_smem(NT, NPL)}
 #define CK(K) \
-    {CL_NT * (K), CL_NE, CL_NT, (int64_t)(K) * CL_NT * CL_NE, solve_cluster_kernel<false>, solve_cluster_kernel<true>, 1, 0, (K)}
+    {CL_NT * (K), CL_NE, CL_NT, (int64_t)(K) * CL_NT * CL_NE, solve_cluster_kernel<false>, solve_cluster_kernel<true>, 1, 0, (K), false}
 // Ascending capacity.  Every padding slot of a subproblem costs as much as a
 // real entry, so the ladder is dense (<= 25% steps) where the F side's and the
 // W side's subproblem sizes concentrate (SURVEY.md §8(d) size profiles).
@@ -1499,7 +1528,7 @@ const FastKernel kFast[] = {
     CK(2),      CK(3),      CK(4),      CK(5),      CK(6),      CK(7),      CK(8),      CK(10),
     CK(12),     CK(14),     CK(16),
     // unbounded: the cooperative long-row kernel (klnmf_solve_coop, schedule built by the caller)
-    {CL_NT, CL_NE, CL_NT, -1, nullptr, nullptr, 1, 0, -1},
+    {CL_NT, CL_NE, CL_NT, -1, nullptr, nullptr, 1, 0, -1, false},
 };
 #undef WK
 #undef BK
@@ -1570,6 +1599,7 @@ static cudaError_t ensure_nonportable(const void *fn) {
 static size_t fast_kernel_smem(const FastKernel &k, int32_t rp) {
     if (k.cluster != 0) return slice_smem(rp);
     return sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt +
+           (k.roff_smem ? sizeof(int) * (size_t)k.ring_entries * (size_t)k.nt : 0) +
            2 * sizeof(float) * (size_t)k.gpb * (size_t)(rp | 1) + (size_t)k.gpb * MAX_CHUNKS + 16;
 }
 
@@ -1671,7 +1701,8 @@ extern "C" int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, v
         return 0;
     }
     const int64_t blocks = (args->n_items + k.gpb - 1) / k.gpb;
-    const size_t ring = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt;
+    const size_t ring = sizeof(float4) * (size_t)ring_stages(k.ring_entries) * (size_t)k.ring_entries * (size_t)k.nt +
+                        (k.roff_smem ? sizeof(int) * (size_t)k.ring_entries * (size_t)k.nt : 0);
     const size_t smem = ring + 2 * sizeof(float) * (size_t)k.gpb * (size_t)(args->rp | 1) +
                         (args->order_mode != KLNMF_ORDER_SHARED ? (size_t)k.gpb * MAX_CHUNKS : 0) + 16;
     if (smem > SMEM_OPTIN) KLNMF_CHECK(ensure_smem((const void *)fn, smem));
