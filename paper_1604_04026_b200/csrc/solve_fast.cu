@@ -449,9 +449,18 @@ constexpr int warp_minb(int npl) {
 #define KLNMF_ROFF_SMEM 1
 #endif
 constexpr bool warp_roff_smem(int npl) { return KLNMF_ROFF_SMEM && (npl <= 7 || npl == 10 || npl == 14); }
+// Threads per warp-kernel block.  One warp per block (32): a warp that
+// finishes its subproblems releases its slot at once instead of idling until
+// the slowest warp of its block is done; the row sums and the visit map are
+// then read through L1 instead of being staged per block.
+#ifndef KLNMF_WARP_NT
+#define KLNMF_WARP_NT 32
+#endif
+constexpr int WARP_NT = KLNMF_WARP_NT;
+constexpr bool WARP_STAGE_SUMS = WARP_NT >= 128;  // row sums / visit map staged in shared memory
 template <int L, int NPL, bool CTR>
-__global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const klnmf_solve_args_t a) {
-    constexpr int NT = 128;
+__global__ void __launch_bounds__(WARP_NT, warp_minb(NPL) * (128 / WARP_NT)) solve_warp_kernel(const klnmf_solve_args_t a) {
+    constexpr int NT = WARP_NT;
     constexpr int GPB = NT / L;  // groups per block
     constexpr int STAGES = ring_stages(NPL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -461,9 +470,11 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
     float *xs_all = reinterpret_cast<float *>(sroff + (RS ? NPL * NT : 0));  // [GPB][2][rps]
     // counter order only: [GPB][MAX_CHUNKS] visit order of each group's chunks
     uint8_t *cord_all = reinterpret_cast<uint8_t *>(xs_all + GPB * 2 * (a.rp | 1));
-    __shared__ double ssum[KMAX_RP];  // fixed-factor row sums by position
-    __shared__ int pin[KMAX_RP];      // visit position -> stored position (perm_in)
+    __shared__ double ssum_s[WARP_STAGE_SUMS ? KMAX_RP : 1];  // fixed-factor row sums by position
+    __shared__ int pin_s[WARP_STAGE_SUMS ? KMAX_RP : 1];      // visit position -> stored position (perm_in)
     __shared__ double tots[GPB][NV];  // reduced partial sums of each group
+    const double *ssum = WARP_STAGE_SUMS ? ssum_s : a.sum_pos;
+    const int *pin = WARP_STAGE_SUMS ? pin_s : a.perm_in;
 
     const int tid = threadIdx.x;
     const int grp = tid / L;
@@ -476,11 +487,13 @@ __global__ void __launch_bounds__(128, warp_minb(NPL)) solve_warp_kernel(const k
     double *tot = tots[grp];
     const int64_t slot = (int64_t)blockIdx.x * GPB + grp;
     const bool valid = slot < a.n_items;
-    for (int k = tid; k < r; k += NT) {
-        ssum[k] = a.sum_pos[k];
-        pin[k] = a.perm_in[k];
+    if (WARP_STAGE_SUMS) {
+        for (int k = tid; k < r; k += NT) {
+            ssum_s[k] = a.sum_pos[k];
+            pin_s[k] = a.perm_in[k];
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (!__any_sync(FULL_MASK, valid)) return;
 
     PhaseClock ph;
@@ -1507,7 +1520,7 @@ struct FastKernel {
 };
 
 #define WK(L, NPL) \
-    {L, NPL, 128, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL, false>, solve_warp_kernel<L, NPL, true>, 128 / (L), NPL, 0, \
+    {L, NPL, WARP_NT, (int64_t)(L) * (NPL), solve_warp_kernel<L, NPL, false>, solve_warp_kernel<L, NPL, true>, WARP_NT / (L), NPL, 0, \
      warp_roff_smem(NPL)}
 #define BK(NT, NPL) \
     {NT, NPL, NT, (int64_t)(NT) * (NPL), solve_block_kernel<NT, NPL, false>, solve_block_kernel<NT, NPL, true>, 1, NPL, 0, \
