@@ -1279,7 +1279,7 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
             u[e] = vi[e] = 0.0;
         }
     }
-    int offs_r[KLNMF_CL_OFF_SMEM ? 1 : NS];
+    [[maybe_unused]] int offs_r[KLNMF_CL_OFF_SMEM ? 1 : NS];
     auto offs = [&](int e) -> int & {
         if constexpr (KLNMF_CL_OFF_SMEM) return Offs[e * NT + tid];
         else return offs_r[e];
@@ -1328,7 +1328,6 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         cp_commit();
         // spilled entries: stage the chunk's slice next to their state
         // (each thread stages and later reads only its own records)
-#pragma unroll 4
         if (cn > spill0)
             spill_stage(UVg, UVm, spill0 + tid, cn, NT, fixed, a.side.idx + base, a.side.n_fix, rp, pc);
         cp_wait<0>();

@@ -21,6 +21,13 @@ KEYS = [
     ("launch__block_size", "block"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1/TEX throughput % peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed", "smem wavefronts % peak"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ldgsts.sum", "LDGSTS sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ldgsts.sum", "LDGSTS requests"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % peak"),
+    ("l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed", "LSU writeback active %"),
 ]
 STALLS = "smsp__average_warps_issue_stalled_"
 

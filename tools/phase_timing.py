@@ -15,7 +15,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-os.environ["KLNMF_LIB"] = str(ROOT / "paper_1604_04026_b200" / "libklnmf_phase.so")
+os.environ.setdefault("KLNMF_LIB", str(ROOT / "paper_1604_04026_b200" / "libklnmf_phase.so"))
 sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
