@@ -315,6 +315,10 @@ int klnmf_upload_f64_as_f32(const double *src_host, int64_t n, float *dst_dev, v
 int klnmf_upload_f64(const double *src_host, int64_t n, double *dst_dev, void *stream);
 int klnmf_download_f32_as_f64(const float *src_dev, int64_t n, double *dst_host, void *stream);
 int klnmf_download_f64(const double *src_dev, int64_t n, double *dst_host, void *stream);
+/* min and max of a host array on the host threads (no device work): the
+ * fp32 mode's range check of V, which the reference's SparseMatrix
+ * validation (sparse.py:29-77) has no counterpart for */
+int klnmf_host_minmax_f64(const double *src_host, int64_t n, double *lo_out, double *hi_out);
 
 /* Device-side synthetic corpus (the planted-topic model of synth.py, drawn
  * with counter-based Philox streams).  Fills col_ptr

@@ -68,6 +68,7 @@ EXPORTS = (
     "klnmf_factor_stats",
     "klnmf_upload_i64_as_i32",
     "klnmf_upload_f64_as_f32",
+    "klnmf_host_minmax_f64",
     "klnmf_upload_f64",
     "klnmf_download_f32_as_f64",
     "klnmf_download_f64",
@@ -180,6 +181,7 @@ _SIGS = {
     "klnmf_factor_stats": ([P, I64, I32, I32, INT, P, P], INT),
     "klnmf_upload_i64_as_i32": ([P, I64, P, P], INT),
     "klnmf_upload_f64_as_f32": ([P, I64, P, P], INT),
+    "klnmf_host_minmax_f64": ([P, I64, P, P], INT),
     "klnmf_upload_f64": ([P, I64, P, P], INT),
     "klnmf_download_f32_as_f64": ([P, I64, P, P], INT),
     "klnmf_download_f64": ([P, I64, P, P], INT),

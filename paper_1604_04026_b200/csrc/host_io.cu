@@ -9,6 +9,7 @@
 // device-side cast.
 #include <algorithm>
 #include <mutex>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -95,6 +96,35 @@ static int upload_narrow(const Src *src, int64_t n, Dst *dst_dev, cudaStream_t s
     }
     KLNMF_CHECK(cudaEventSynchronize(S->done[0]));
     KLNMF_CHECK(cudaEventSynchronize(S->done[1]));
+    return 0;
+}
+
+// min and max of a host array on the host threads (the fp32 mode's range
+// check of V before anything is uploaded; numpy's single-threaded min()/max()
+// took 50 ms of a C4 plan build).  NaN compares false and is skipped.
+extern "C" int klnmf_host_minmax_f64(const double *src_host, int64_t n, double *lo_out, double *hi_out) {
+    if (n <= 0) return set_error_msg(1, "klnmf_host_minmax_f64: empty array");
+    const int nt = n_threads();
+    std::vector<double> lo((size_t)nt + 1, src_host[0]), hi((size_t)nt + 1, src_host[0]);
+    std::atomic<int> slot{0};
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        double l = src_host[a], h = src_host[a];
+        for (int64_t i = a; i < b; ++i) {
+            const double v = src_host[i];
+            l = v < l ? v : l;
+            h = v > h ? v : h;
+        }
+        const int k = slot.fetch_add(1);
+        lo[(size_t)k] = l;
+        hi[(size_t)k] = h;
+    });
+    double l = lo[0], h = hi[0];
+    for (int k = 0; k < slot.load(); ++k) {
+        l = lo[(size_t)k] < l ? lo[(size_t)k] : l;
+        h = hi[(size_t)k] > h ? hi[(size_t)k] : h;
+    }
+    *lo_out = l;
+    *hi_out = h;
     return 0;
 }
 
