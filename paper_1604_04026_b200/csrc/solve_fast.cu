@@ -1063,6 +1063,10 @@ __device__ __forceinline__ void st_async_v2(unsigned raddr, double x, double y, 
                  : "memory");
 }
 
+#ifndef KLNMF_CL_SUM_UNROLL
+#define KLNMF_CL_SUM_UNROLL 4
+#endif
+constexpr int CL_SUM_UNROLL = KLNMF_CL_SUM_UNROLL;
 constexpr int CL_MAXK = 16;  // largest cluster
 // Per-CTA inbox of the cluster all-reduce: round parity x source CTA x value.
 #ifdef KLNMF_CHECKED
@@ -1120,6 +1124,8 @@ struct ClusterReducer {
 #endif
                 if (lane < NV) {
                     double t = 0.0;
+                    // the peers' partials are loaded in batches ahead of the ordered sum
+                    _Pragma("unroll CL_SUM_UNROLL")
                     for (int c = 0; c < k; ++c) t += P.box[b][c][lane];
                     R.tot[buf][lane] = t;
                 }
@@ -1161,6 +1167,51 @@ __device__ __forceinline__ void coop_backoff() {
     if (KLNMF_COOP_SLEEP_NS > 0) __nanosleep(KLNMF_COOP_SLEEP_NS);
 }
 
+// Lane `lane`'s share of one value's sum over the G slots of a cooperative
+// reduction round (slots c = lane, lane + 32, ... in ascending order).
+// KLNMF_COOP_RD slots per lane are requested before the first tag is tested,
+// so a wide group (G up to 512: 16 slots per lane) pays one L2 round trip per
+// batch instead of one per slot.  Out of line (KLNMF_COOP_NOINLINE): the
+// batch's registers do not add to the pressure of the slice loop.
+#ifndef KLNMF_COOP_RD
+#define KLNMF_COOP_RD 2
+#endif
+#ifndef KLNMF_COOP_NOINLINE
+#define KLNMF_COOP_NOINLINE 1
+#endif
+#if KLNMF_COOP_NOINLINE
+#define KLNMF_COOP_SUM_ATTR __noinline__
+#else
+#define KLNMF_COOP_SUM_ATTR __forceinline__
+#endif
+__device__ KLNMF_COOP_SUM_ATTR double coop_sum_column(const unsigned long long *col, int G, unsigned tag, int lane) {
+    double acc = 0.0;
+    for (int c0 = 0; c0 < G; c0 += 32 * KLNMF_COOP_RD) {
+        ulonglong2 q[KLNMF_COOP_RD];
+#pragma unroll
+        for (int b2 = 0; b2 < KLNMF_COOP_RD; ++b2) {
+            const int c = c0 + 32 * b2 + lane;
+            if (c < G) q[b2] = ld_relaxed_v2(col + 2 * c);
+        }
+#pragma unroll
+        for (int b2 = 0; b2 < KLNMF_COOP_RD; ++b2) {
+            const int c = c0 + 32 * b2 + lane;
+            double x = 0.0;
+            if (c < G) {
+                while ((unsigned)q[b2].x != tag || (unsigned)q[b2].y != tag) {
+                    // a newer tag means round n+2 overwrote this slot before it was read
+                    kcheck((unsigned)q[b2].x <= tag && (unsigned)q[b2].y <= tag, 6);
+                    coop_backoff();
+                    q[b2] = ld_relaxed_v2(col + 2 * c);
+                }
+                x = __longlong_as_double((long long)((q[b2].x & 0xffffffff00000000ull) | (q[b2].y >> 32)));
+            }
+            acc += x;
+        }
+    }
+    return acc;
+}
+
 struct CoopReducer {
     GroupRed &R;
     unsigned long long *slots;  // [2][NV][CL_MAXG][2] tagged words
@@ -1196,22 +1247,7 @@ struct CoopReducer {
         __syncthreads();
         for (int vw = w; vw < NV; vw += CL_NT / 32) {  // warp vw sums value vw (any CTA width)
             const unsigned long long *col = slots + ((size_t)b * NV + vw) * CL_MAXG * 2;
-            double acc = 0.0;
-            for (int c0 = 0; c0 < G; c0 += 32) {
-                const int c = c0 + lane;
-                double x = 0.0;
-                if (c < G) {
-                    ulonglong2 q = ld_relaxed_v2(col + 2 * c);
-                    while ((unsigned)q.x != (unsigned)tag || (unsigned)q.y != (unsigned)tag) {
-                        // a newer tag means round n+2 overwrote this slot before it was read
-                        kcheck((unsigned)q.x <= (unsigned)tag && (unsigned)q.y <= (unsigned)tag, 6);
-                        coop_backoff();
-                        q = ld_relaxed_v2(col + 2 * c);
-                    }
-                    x = __longlong_as_double((long long)((q.x & 0xffffffff00000000ull) | (q.y >> 32)));
-                }
-                acc += x;
-            }
+            double acc = coop_sum_column(col, G, (unsigned)tag, lane);
             acc = warp_sum(acc);
             if (lane == 0) R.tot[buf][vw] = acc;
         }

@@ -113,3 +113,24 @@ def test_memory_accounting_is_sparse(cuda_ok, precision):
     kb.factorize(V, kb.NmfConfig(rank=4, max_outer_iters=5, precision=precision), ledger=ledger)
     assert ledger.peak_bytes > 0
     assert ledger.max_single_bytes < 8 * V.shape[0] * V.shape[1]
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_unlogged_run_queues_ahead_and_matches_the_logged_one(cuda_ok, precision):
+    # without a log or a time budget factorize does not wait for the device
+    # between iterations (solver.py: sync_each); the iterates must not change.
+    # Enough iterations for the half-step graphs to be captured and replayed
+    # while earlier iterations are still in flight.
+    import paper_1604_04026_b200 as kb
+
+    V = _sparse_counts(11, 300, 500, 0.2)
+    pair = kb.init_factors(300, 500, 8, seed=6, mean_v=1.0)
+    kw = dict(rank=8, max_outer_iters=9, rel_obj_tol=0.0, precision=precision, seed=3)
+    logged = kb.factorize(V, kb.NmfConfig(log_objectives=True, **kw), factors0=pair)
+    quiet = kb.factorize(V, kb.NmfConfig(log_objectives=False, **kw), factors0=pair)
+    assert quiet.iterations_run == logged.iterations_run == 9 and len(quiet.log) == 0
+    assert np.array_equal(quiet.factors.w.values, logged.factors.w.values)
+    assert np.array_equal(quiet.factors.f.values, logged.factors.f.values)
+    assert (quiet.stats.inner_iters, quiet.stats.cap_hits, quiet.stats.degenerate) == (
+        logged.stats.inner_iters, logged.stats.cap_hits, logged.stats.degenerate)
+    assert quiet.solve_seconds > 0.0
