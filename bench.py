@@ -556,7 +556,14 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": dbytes,
                          "step_achieved_gbs": it_bytes / (ms_per_step * 1e-3) / 1e9,
                          "step_frac": it_bytes / (ms_per_step * 1e-3) / 1e9 / peak,
-                         "step_algorithmic_bytes": it_bytes},
+                         "step_algorithmic_bytes": it_bytes,
+                         # the other measured bound of the step: every entry and 4-coordinate
+                         # chunk is one 16-byte cp.async lane request; a fully divergent warp instruction
+                         # costs 33.4 L1/TEX cycles per SM (profiles/r05_gather_microbench.md)
+                         "l1tex_gather_floor_ms": 2.0 * V.nnz * ((r + 3) // 4) / 32.0 * 33.4 / (148 * 1.965e9) * 1e3
+                         / world,
+                         "l1tex_gather_frac": (2.0 * V.nnz * ((r + 3) // 4) / 32.0 * 33.4 / (148 * 1.965e9) * 1e3
+                                               / world) / ms_per_step},
             "kernels": kernel_table,
             "kernel_timing": "kernels/roofline: per-launch durations from an instrumented pass with the buckets "
                              "launched one at a time (continuing the same trajectory); the timed steps run "
