@@ -198,6 +198,17 @@ typedef struct {
      * t_out / peer_t written through tmap into the other side's entry order
      * (coalesced reads at every subproblem start; scattered stores). */
     int32_t t_scatter;
+    /* fp32 mode, long-row kernels: n_fix words, bit c set iff the fixed
+     * factor's row has a nonzero among its stored positions 4c .. 4c+3
+     * (klnmf_chunk_masks, computed at the start of the half-step).  A slice
+     * gathers a row's 16-byte chunk only when its bit is set -- an all-zero
+     * chunk is zero-filled without a memory request, which is bit-identical.
+     * NULL = gather everything.  slice_words: 4 * nnz 16-bit words of work
+     * space for the slices' per-thread transposed masks (a slice uses the
+     * range of its own entries; slices shorter than 64 entries per chunk
+     * gather everything). */
+    const uint32_t *fixed_mask;
+    uint16_t *slice_words;
 } klnmf_solve_args_t;
 
 #define KLNMF_ORDER_SHARED 0
@@ -217,6 +228,10 @@ int klnmf_mu_update_dev(const klnmf_side_t *side, const double *fixed, double *m
 /* fp32-storage / fp64-arithmetic solver.  kernel_id selects the bucket kernel:
  * lanes-per-subproblem L and entries-per-lane NPL (klnmf_fast_kernel_info). */
 int klnmf_solve_fast(const klnmf_solve_args_t *args, int kernel_id, void *stream);
+/* out[i] bit c = the (n_fix, rp) fp32 factor's row i has a nonzero among
+ * positions 4c .. 4c+3 (c < ceil(r/4) <= 32, i.e. r <= 128; larger ranks: all
+ * bits set).  For klnmf_solve_args_t.fixed_mask. */
+int klnmf_chunk_masks(const float *fixed, int64_t n_fix, int32_t rp, int32_t r, uint32_t *out, void *stream);
 /* Sets the launch attributes of every fp32 kernel for padded rank rp once
  * (call before capturing launches into a CUDA graph). */
 int klnmf_prepare_fast(int32_t rp);

@@ -54,6 +54,7 @@ EXPORTS = (
     "klnmf_solve_coop",
     "klnmf_row_sums_exact",
     "klnmf_row_sums_fast",
+    "klnmf_chunk_masks",
     "klnmf_layout_to_device",
     "klnmf_layout_to_device_f32src",
     "klnmf_layout_from_device",
@@ -132,6 +133,8 @@ class SolveArgs(ctypes.Structure):
         ("peer_moving", P),
         ("peer_t", P),
         ("t_scatter", I32),
+        ("fixed_mask", P),
+        ("slice_words", P),
     ]
 
 
@@ -167,6 +170,7 @@ _SIGS = {
     "klnmf_solve_coop": ([ctypes.POINTER(SolveArgs), P, I32, I32, P, I64, P], INT),
     "klnmf_row_sums_exact": ([P, I64, I32, I32, P, P], INT),
     "klnmf_row_sums_fast": ([P, I64, I32, I32, P, P], INT),
+    "klnmf_chunk_masks": ([P, I64, I32, I32, P, P], INT),
     "klnmf_layout_to_device": ([P, I64, I64, P, I32, P, INT, P], INT),
     "klnmf_layout_to_device_f32src": ([P, I64, I64, P, I32, P, P], INT),
     "klnmf_layout_from_device": ([P, I64, I64, P, I32, INT, P, P], INT),

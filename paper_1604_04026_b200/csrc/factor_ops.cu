@@ -185,6 +185,31 @@ extern "C" int klnmf_layout_from_device_f32(const float *src, int64_t r, int64_t
     return 0;
 }
 
+// Chunk nonzero masks of a factor's rows (klnmf_solve_args_t.fixed_mask):
+// one warp per row, lane c tests the 16-byte chunk c.
+__global__ void chunk_masks_kernel(const float *fac, int64_t n_items, int32_t rp, int32_t r, uint32_t *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (row >= n_items) return;
+    bool nz = false;
+    if (4 * lane < r) {
+        const float4 v = *reinterpret_cast<const float4 *>(fac + row * rp + 4 * lane);
+        nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) out[row] = r > 128 ? 0xffffffffu : m;
+}
+
+extern "C" int klnmf_chunk_masks(const float *fixed, int64_t n_fix, int32_t rp, int32_t r, uint32_t *out,
+                                 void *stream) {
+    if (n_fix <= 0) return 0;
+    if (rp % 4 != 0) return set_error_msg(1, "klnmf_chunk_masks: rp must be a multiple of 4");
+    const int wpb = 8;
+    chunk_masks_kernel<<<(unsigned)((n_fix + wpb - 1) / wpb), 32 * wpb, 0, as_stream(stream)>>>(fixed, n_fix, rp, r, out);
+    KLNMF_CHECK_LAUNCH("klnmf_chunk_masks");
+    return 0;
+}
+
 extern "C" int klnmf_row_sums_fast(const float *fac, int64_t n_items, int32_t rp, int32_t r,
                                    double *out, void *stream) {
     cudaStream_t st = as_stream(stream);

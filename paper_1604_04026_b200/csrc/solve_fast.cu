@@ -291,7 +291,7 @@ struct TReduce {
 // store, 5 product store, 6 cooperative slot overwritten before it was read
 // (parity reuse violated), 7 arrival counter two rounds ahead, 8 spill
 // record out of range, 9 non-finite / negative entry state, 10 cluster inbox
-// round mismatch.
+// round mismatch, 11 a chunk skipped by its mask holds a nonzero.
 #ifdef KLNMF_CHECKED
 __device__ unsigned long long g_check[2];
 __device__ __forceinline__ void kcheck(bool ok, unsigned code) {
@@ -1256,6 +1256,30 @@ struct CoopReducer {
     }
 };
 
+// Per-thread chunk masks of a slice (klnmf_solve_args_t.fixed_mask): word
+// [chunk][tid] holds bit e = "resident entry e of this thread has a nonzero
+// in that chunk of its fixed-factor row".  Built once per slice from the
+// per-row masks into klnmf_solve_args_t.slice_words (8 bytes of word space
+// per entry: the slice's own range), read back one word per thread and chunk.
+// Out of line: the 16 row masks are live only here.
+constexpr int SLICE_MASK_CHUNKS = 32;  // one bit per chunk in the per-row words: r <= 128
+__device__ __noinline__ void slice_masks_build(uint16_t *words, const uint32_t *fixed_mask, const int32_t *idx,
+                                               int64_t cn, int nchunks) {
+    const int tid = threadIdx.x;
+    uint32_t m[CL_NE];
+#pragma unroll
+    for (int e = 0; e < CL_NE; ++e) {
+        const int64_t i = tid + (int64_t)e * CL_NT;
+        m[e] = i < cn ? __ldg(fixed_mask + idx[i]) : 0u;
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        unsigned w = 0;
+#pragma unroll
+        for (int e = 0; e < CL_NE; ++e) w |= ((m[e] >> c) & 1u) << e;
+        words[c * CL_NT + tid] = (uint16_t)w;
+    }
+}
+
 // One subproblem's slice on one CTA (rank cq of the k CTAs sharing it).
 template <bool CTR, typename Reducer>
 __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t slot, int cq, int k, Reducer &reduce,
@@ -1301,6 +1325,15 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
 
     for (int kk = tid; kk < r; kk += NT) xs[kk] = moving[j * rp + a.perm_in[kk]];
 
+    // chunk masks of this thread's resident entries (each thread writes and
+    // reads only its own words): all-zero slices of the fixed factor are not
+    // gathered
+    const int nchunks = (r + C - 1) / C;
+    uint16_t *mwords = a.slice_words + 4 * base;  // 8 bytes of word space per entry of the slice
+    const bool masked = a.fixed_mask != nullptr && a.slice_words != nullptr && 4 * cn >= (int64_t)nchunks * NT &&
+                        nchunks <= SLICE_MASK_CHUNKS && NR + NS <= 16;
+    if (masked) slice_masks_build(mwords, a.fixed_mask, a.side.idx + base, cn, nchunks);
+
     double u[NR], vi[NR];
     int off[NR];
 #pragma unroll
@@ -1342,7 +1375,6 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
         UVg[i].uv = make_double2(uu, vv);
     }
     const unsigned cache_s = (unsigned)__cvta_generic_to_shared(cache) + 16u * tid;
-    const int nchunks = (r + C - 1) / C;
     constexpr bool counter = CTR;
     if (counter && tid == 0) chunk_order(a.order_seed, *a.order_iter, (uint32_t)j, a.order_side, nchunks, cord);
     __syncthreads();
@@ -1350,18 +1382,36 @@ __device__ __forceinline__ void solve_slice(const klnmf_solve_args_t &a, int64_t
 
     Counters cnt;
     int buf = 0, cur = 0;
+    // this chunk's mask word, loaded one chunk ahead
+    unsigned mnext = masked ? (unsigned)mwords[(counter ? (int)cord[0] : 0) * NT + tid] : 0xffffu;
     for (int ch = 0; ch < nchunks; ++ch) {
         ph.count(11);
         const int pc = counter ? (int)cord[ch] : ch;  // physical chunk
-        // gather this chunk of every resident entry once (own slots only)
+        const unsigned mw = mnext;
+        if (masked && ch + 1 < nchunks) mnext = (unsigned)mwords[(counter ? (int)cord[ch + 1] : ch + 1) * NT + tid];
+        // gather this chunk of every resident entry once (own slots only);
+        // entries whose row is all zero in this chunk are zero-filled without a request
 #pragma unroll
         for (int e = 0; e < NR; ++e)
-            if (e < ne) cp_async16(cache_s + 16u * NT * e, fixed + max(off[e], 0) + pc * C, off[e] >= 0);
+            if (e < ne)
+                cp_async16(cache_s + 16u * NT * e, fixed + max(off[e], 0) + pc * C, off[e] >= 0 && ((mw >> e) & 1u));
 #pragma unroll
         for (int e = 0; e < NS; ++e)
             if (NR + e < ne)
-                cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs(e), 0) + pc * C, offs(e) >= 0);
+                cp_async16(cache_s + 16u * NT * (NR + e), fixed + max(offs(e), 0) + pc * C,
+                           offs(e) >= 0 && ((mw >> (NR + e)) & 1u));
         cp_commit();
+#ifdef KLNMF_CHECKED  // a skipped chunk really is all zero (code 11)
+        if (masked) {
+            for (int e = 0; e < NR + NS; ++e) {
+                const int64_t i = tid + (int64_t)e * NT;
+                if (e < ne && i < cn && !((mw >> e) & 1u)) {
+                    const float4 z = ldg_f4(fixed + (int64_t)a.side.idx[base + i] * rp + pc * C);
+                    kcheck(z.x == 0.f && z.y == 0.f && z.z == 0.f && z.w == 0.f, 11);
+                }
+            }
+        }
+#endif
         // spilled entries: stage the chunk's slice next to their state
         // (each thread stages and later reads only its own records)
         if (cn > spill0)

@@ -346,6 +346,19 @@ class DevicePlan:
             self._perm_host = torch.zeros(4, self.rp, dtype=torch.int32).pin_memory()
             self._perm_event = None
             self.use_graphs = True
+            # per-row chunk nonzero masks of the fixed factor (long-row kernels; KLNMF_SLICE_MASKS=0: off)
+            self.slice_masks = os.environ.get("KLNMF_SLICE_MASKS", "1") != "0"
+            self._fixed_mask = torch.zeros(max(self.n, self.m), dtype=torch.int32, device=dev)
+            self._track("fixed_mask", self._fixed_mask)
+            self._slice_words = None
+            if self.fp32 and self.slice_masks and self.r <= 128:
+                lanes_of = {k[0]: k[2] for k in self.fast_kernels}
+                coop_id = self._stream_kernel_id()
+                if any(c > 0 and (kid == coop_id or lanes_of.get(kid, 0) > 256)
+                       for sd in self.sides.values() for kid, _, c in sd.buckets):
+                    # 8 bytes of mask-word space per entry, only when a side has long rows
+                    self._slice_words = torch.empty(4 * max(self.nnz, 1), dtype=torch.int16, device=dev)
+                    self._track("slice_words", self._slice_words)
             self._capturing = False
             # streams (and fork/join events) for running independent buckets
             # concurrently; concurrent = False launches them one at a time
@@ -874,6 +887,16 @@ class DevicePlan:
         main = self.stream_ptr
         buckets = [b for b in side.buckets if b[2] > 0]
         coop_kid = self._stream_kernel_id()
+        if self._slice_words is not None:
+            # chunk nonzero masks of the fixed factor's rows for the long-row
+            # kernels (cluster widths have more than 256 lanes): all-zero
+            # 16-byte chunks are not gathered
+            lanes_of = {k[0]: k[2] for k in self.fast_kernels}
+            if any(kid == coop_kid or lanes_of.get(kid, 0) > 256 for kid, _, _ in buckets):
+                _lib.call("klnmf_chunk_masks", a.fixed, self.factors[fixed_name].shape[0], self.rp, self.r,
+                          self._fixed_mask.data_ptr(), main)
+                a.fixed_mask = self._fixed_mask.data_ptr()
+                a.slice_words = self._slice_words.data_ptr()
         # the buckets are independent (disjoint outputs, atomic stats) and
         # fork over several streams, so one bucket's last partial wave and
         # the few-subproblem buckets overlap the others;

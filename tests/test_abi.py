@@ -39,7 +39,7 @@ def test_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.Side) == 48
     # side, 12 pointers, r/rp, 5 doubles, inner_cap, stats, order mode/side, order seed, order_iter,
     # max_passes/n_peers, peer pointers, t_scatter (+ padding)
-    assert ctypes.sizeof(_lib.SolveArgs) == 48 + 8 * 12 + 8 + 8 * 5 + 8 + 8 + 8 + 8 + 8 + 8 + 16 + 8
+    assert ctypes.sizeof(_lib.SolveArgs) == 48 + 8 * 12 + 8 + 8 * 5 + 8 + 8 + 8 + 8 + 8 + 8 + 16 + 8 + 16  # ... t_scatter (padded), fixed_mask, slice_words
     # and as the C compiler lays it out
     lib = _lib.load()
     assert lib.klnmf_sizeof_solve_args() == ctypes.sizeof(_lib.SolveArgs)
