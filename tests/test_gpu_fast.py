@@ -422,3 +422,48 @@ def test_coop_spill_beyond_on_chip_capacity(cuda_ok):
     mg, mo, tg, to, sg, so = _compare_half_step(plan, "F", ids, 0.01, 0.0)
     _check(mg, mo, tg, to, "spill")
     _check_stats(sg, so)
+
+
+def test_long_row_gather_skip_is_bit_identical(cuda_ok, monkeypatch):
+    """The long-row kernels do not gather 16-byte chunks of the fixed factor
+    that klnmf_chunk_masks marks all zero (zero-filled instead): with a fixed
+    factor whose chunks are mostly zero, cluster and cooperative rows give the
+    same bits with the masks on and off, and match the fp32 oracle."""
+    import paper_1604_04026_b200 as kb
+    from paper_1604_04026_b200 import _lib
+    from paper_1604_04026_b200.plan import DevicePlan
+
+    per_cta, _, _ = _lib.coop_info(12)
+    rng = np.random.default_rng(21)
+    # columns for a 2-CTA and a 5-CTA cluster, the cooperative kernel, and short ones
+    sizes = [per_cta + per_cta // 2, 4 * per_cta + 100, 17 * per_cta + 33, 300, 5]
+    n = 20 * per_cta
+    rows, cols = [], []
+    for j, s_ in enumerate(sizes):
+        rows.append(np.sort(rng.choice(n, size=s_, replace=False)))
+        cols.append(np.full(s_, j))
+    rows = np.concatenate(rows)
+    V = kb.SparseMatrix.from_coo(n, len(sizes), rows, np.concatenate(cols),
+                                 rng.integers(1, 6, size=rows.shape[0]).astype(np.float64))
+    r = 10  # three chunks, the last one partial
+    w0 = rng.random((r, n)).astype(np.float32).astype(np.float64)
+    ids = rng.permutation(r)
+    # zero whole stored chunks of most rows (storage order = the visit order ids)
+    for c in range(3):
+        dead = rng.random(n) < 0.7
+        coords = ids[4 * c: 4 * c + 4]
+        w0[np.ix_(coords, np.nonzero(dead)[0])] = 0.0
+    f0 = rng.random((r, len(sizes))).astype(np.float32).astype(np.float64)
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KLNMF_SLICE_MASKS", flag)
+        plan = DevicePlan(V, r, "fp32")
+        assert (plan._slice_words is not None) == (flag == "1")
+        plan.set_factors(w0, f0, order=ids)
+        mg, mo, tg, to, sg, so = _compare_half_step(plan, "F", ids, 0.01, 0.0)
+        _check(mg, mo, tg, to, f"gather skip masks={flag}")
+        _check_stats(sg, so)
+        outs[flag] = (mg, tg, sg.inner_iters)
+    assert np.array_equal(outs["1"][0], outs["0"][0])
+    assert np.array_equal(outs["1"][1], outs["0"][1])
+    assert outs["1"][2] == outs["0"][2]
